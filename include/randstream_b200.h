@@ -1,0 +1,149 @@
+/*
+ * randstream_b200.h -- C ABI of the B200-native bulk stream-fill library
+ * (paper_2605_05099_b200/librandstream_b200.so).
+ *
+ * The reference (`randstream`, pure Python) has no FFI of its own; these entry
+ * points replace the Python operator it exposes for this path and are what a
+ * ctypes / cffi binding of that operator binds (INTEGRATION.md shows the stub):
+ *
+ *   rs_fill          replaces Rng.fill(dist, params, n)
+ *                    /root/reference/pkg/src/randstream/rng.py:223-241
+ *                    -> continuous.fill  continuous.py:413-431
+ *                    -> discrete.fill    discrete.py:103-111
+ *   rs_fill_streams  replaces the per-stream loop
+ *                    `create(engine, seed, spawn_key=(j,)).fill(...)` over j
+ *                    (state_io.py:13-19 + rng.py:223-241; spawn keys seeding.py:51-61)
+ *   rs_mvn           replaces Rng.mvn(mean, cov, n, layout)  rng.py:273-275,
+ *                    continuous.py:312-336 (the factor L is computed by the caller)
+ *   rs_engine_*      the engine protocol used for stream positioning and the
+ *                    144-word buffer refills: generate (engines/*.py generate),
+ *                    seed (seeding.py:115-116 + engines seed_from), jump/advance
+ *                    (rng.py:135-171, jumps.py:116-126, pcg.py:41-55, ranlux.py:90-93)
+ *   rs_last_error    replaces the per-handle error slot (rng.py:38-52, state_io.py:45-47)
+ *
+ * Conventions: plain pointers and sizes only. `cuda_stream` is a cudaStream_t
+ * passed as void* (NULL = legacy default stream). Output pointers may be
+ * device memory (written in place, stream-ordered) or host memory (the
+ * library stages through device scratch and copies back before returning).
+ * All validation happens before any state change; on error the stream is
+ * untouched and rs_last_error() describes the failure.
+ */
+#ifndef RANDSTREAM_B200_H
+#define RANDSTREAM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_ABI_VERSION 1
+#define RS_BUFFER_CAPACITY 144 /* buffer.py:12 */
+
+typedef enum {
+    RS_OK = 0,
+    RS_ERR_VALUE = 1,       /* ValueError in the reference */
+    RS_ERR_UNSUPPORTED = 2, /* engine/dist not on the device path */
+    RS_ERR_CUDA = 3,
+    RS_ERR_INTERNAL = 4
+} rs_status;
+
+/* engine ids: the reference registry order, engines/__init__.py:11-26 */
+typedef enum {
+    RS_ENG_X256PP = 1,
+    RS_ENG_X256SS = 2,
+    RS_ENG_X128P = 3,
+    RS_ENG_XORO = 4,
+    RS_ENG_PCG64 = 5,
+    RS_ENG_PHILOX = 6,
+    RS_ENG_SQUARES = 7,
+    RS_ENG_SFC64 = 8,
+    RS_ENG_CWG128 = 9,
+    RS_ENG_RANLUX = 10,
+    RS_ENG_CHACHA20 = 11,
+    RS_ENG_X256PP_SIMD = 12,
+    RS_ENG_X256SS_SIMD = 13,
+    RS_ENG_SFC64_SIMD = 14
+} rs_engine;
+
+/* distribution ids (continuous.py:339-359 / discrete.py:95-100 names) */
+typedef enum {
+    RS_DIST_UINT64 = 1,  /* "uint64": iparams[0]=b (0 = raw word), iparams[1]=1 means b = 2^64 */
+    RS_DIST_U01 = 2,     /* "u01"   : f64, mapping per full_mantissa (rng.py:98-106) */
+    RS_DIST_U01F = 3,    /* "u01f"  : f32 from u32 halves, low half first (rng.py:108-115) */
+    RS_DIST_NORM = 4,    /* "norm"  : fparams {mu, var} */
+    RS_DIST_EXP = 5,     /* "exp"   : fparams {beta} */
+    RS_DIST_GAMMA = 6,   /* "gamma" : fparams {alpha, theta} */
+    RS_DIST_BETA = 7,    /* "beta"  : fparams {a, b} */
+    RS_DIST_STDNORM = 8  /* std_norm without the norm epilogue (the mvn z draws, continuous.py:332) */
+} rs_dist;
+
+/* A generator's full logical position (engine words + WordBuffer, buffer.py:17-60).
+ * rs_fill reads it and writes back the post-fill position. */
+typedef struct rs_stream {
+    int32_t engine;         /* rs_engine */
+    int32_t full_mantissa;  /* Rng.full_mantissa (rng.py:59-60) */
+    int32_t bitexact;       /* Rng.bitexact (only affects transform families) */
+    int32_t has_pending;    /* WordBuffer.pending is not None */
+    uint64_t pending;       /* the buffered high half (u32) */
+    uint64_t state[9];      /* engine.get_state() words */
+    uint64_t buf[RS_BUFFER_CAPACITY];
+    int32_t fill;           /* len(WordBuffer.words): 0 or 144 */
+    int32_t cursor;         /* WordBuffer.cursor */
+} rs_stream;
+
+typedef struct rs_fill_result {
+    uint64_t words_consumed;  /* logical 64-bit words taken from the stream */
+    uint64_t tally[6];        /* norm attempts, norm pdf_evals, exp attempts, exp pdf_evals,
+                                 gamma attempts, gamma pdf_evals (continuous.py:32-33) */
+    int32_t tally_seen[3];    /* which of norm/exp/gamma the fill touched */
+    int32_t resync_rounds;    /* extra segment-entry resolution rounds (0 normally) */
+    uint64_t chunks;          /* provisioning rounds used */
+} rs_fill_result;
+
+/* library */
+int32_t rs_abi_version(void);
+const char *rs_last_error(void);                  /* thread-local, "" after a success */
+rs_status rs_init_device(int32_t device);         /* upload constant tables once per device */
+int32_t rs_engine_supported(int32_t engine);      /* 1 if rs_fill runs this engine on the GPU */
+
+/* engine protocol (host-side state bookkeeping; the reference's L1/L1' layer) */
+int32_t rs_engine_state_words(int32_t engine);
+int32_t rs_engine_seed_words(int32_t engine);
+int32_t rs_engine_chunk(int32_t engine);
+rs_status rs_seed_words(const uint64_t *entropy, int32_t n_entropy, const uint64_t *spawn_key,
+                        int32_t n_spawn, uint64_t *out, int32_t n_out);
+rs_status rs_engine_seed(int32_t engine, const uint64_t *entropy, int32_t n_entropy,
+                         const uint64_t *spawn_key, int32_t n_spawn, uint64_t *state_out);
+rs_status rs_engine_seed_from(int32_t engine, const uint64_t *words, uint64_t *state_out);
+rs_status rs_engine_check_state(int32_t engine, const uint64_t *words);
+rs_status rs_engine_generate(int32_t engine, uint64_t *state, uint64_t *out, int32_t n);
+rs_status rs_engine_jump(int32_t engine, uint64_t *state, int32_t k);
+rs_status rs_engine_advance_words(int32_t engine, uint64_t *state, uint64_t words_lo, uint64_t words_hi);
+rs_status rs_pcg_advance(uint64_t *state, uint64_t delta_lo, uint64_t delta_hi);
+
+/* the hot path */
+rs_status rs_fill(rs_stream *stream, int32_t dist, const double *fparams, const uint64_t *iparams,
+                  uint64_t n, void *out, rs_fill_result *result, void *cuda_stream);
+
+/* Launch-only variant for benchmarking/graph capture: same kernels, no host
+ * synchronisation, `stream` is NOT advanced (each call recomputes the same fill). */
+rs_status rs_fill_async(const rs_stream *stream, int32_t dist, const double *fparams,
+                        const uint64_t *iparams, uint64_t n, void *out_device, void *cuda_stream);
+
+/* per-stream mode: out[s][i] = create(engine, seed, spawn_key = prefix + (j0 + s,)).fill(...)[i] */
+rs_status rs_fill_streams(int32_t engine, const uint64_t *seed, int32_t n_seed,
+                          const uint64_t *spawn_prefix, int32_t n_prefix, uint64_t j0,
+                          uint64_t n_streams, int32_t dist, const double *fparams,
+                          const uint64_t *iparams, uint64_t n_per_stream, void *out,
+                          void *cuda_stream);
+
+/* x = mean + z @ L^T with z = n*d std_norm draws from `stream` (row-major (n, d)).
+ * L: d x d row-major (device or host), mean: d (host). layout 0 = "n_d", 1 = "d_n". */
+rs_status rs_mvn(rs_stream *stream, const double *L, const double *mean, int64_t d, uint64_t n,
+                 int32_t layout, double *out, rs_fill_result *result, void *cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

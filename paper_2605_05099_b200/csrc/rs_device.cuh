@@ -1,0 +1,679 @@
+// Device building blocks for the bulk stream-fill kernels (sm_100a).
+//
+//  * engines: xoshiro256**/++, PCG64-DXSM, Philox-4x64-10, sfc64, ranlux++ --
+//    one 64-bit word per next(), same words as the reference generate()
+//    (engines/xorfam.py:88-124, pcg.py:25-39, counter.py:98-121, sfc.py:25-36,
+//    ranlux.py:36-88);
+//  * det_exp / det_log: fdlibm kernels op for op (detmath.py:59-163). The whole
+//    library is compiled with -fmad=false so no multiply-add is contracted:
+//    results are bit-identical to CPython's IEEE doubles;
+//  * parsers: the reference samplers restated as word-at-a-time state machines
+//    (continuous.py:40-93 ziggurats, :183-218 gamma/beta, discrete.py:20-39 Lemire)
+//    so a segment of the word stream can be parsed by one thread. A "boundary"
+//    is the position right after an emitted sample -- the only point where the
+//    reference's call stack carries no state;
+//  * VecWriter: per-lane contiguous runs written with 256-bit stores (STG.256).
+#pragma once
+#include <cstdint>
+
+#include "rs_tables_dev.cuh"
+
+typedef uint64_t u64;
+typedef unsigned int u32;
+
+#define RS_DEV __device__ __forceinline__
+
+RS_DEV u64 rotl64(u64 x, int k) { return (x << k) | (x >> (64 - k)); }
+
+// ----------------------------------------------------------------------------- engines
+
+template <bool SS>
+struct EngX256 {  // xorfam.py:88-124
+    u64 s0, s1, s2, s3;
+    RS_DEV void load(const u64 *p) { s0 = p[0]; s1 = p[1]; s2 = p[2]; s3 = p[3]; }
+    RS_DEV u64 next() {
+        u64 r = SS ? rotl64(s1 * 5ULL, 7) * 9ULL : rotl64(s0 + s3, 23) + s0;
+        u64 t = s1 << 17;
+        s2 ^= s0; s3 ^= s1; s1 ^= s2; s0 ^= s3; s2 ^= t;
+        s3 = rotl64(s3, 45);
+        return r;
+    }
+};
+
+#define RS_PCG_MULT 0xDA942042E4DD58B5ULL
+struct EngPcg {  // pcg.py:25-39 (DXSM of the pre-step state; 64-bit "cheap" multiplier)
+    u64 slo, shi, ilo, ihi;
+    RS_DEV u64 next() {
+        u64 hi = shi, lo = slo | 1ULL;
+        hi ^= hi >> 32;
+        hi *= RS_PCG_MULT;
+        hi ^= hi >> 48;
+        u64 r = hi * lo;
+        u64 nlo = slo * RS_PCG_MULT;
+        u64 nhi = __umul64hi(slo, RS_PCG_MULT) + shi * RS_PCG_MULT;
+        u64 a = nlo + ilo;
+        nhi += ihi + (a < nlo ? 1ULL : 0ULL);
+        slo = a; shi = nhi;
+        return r;
+    }
+    // state <- mul*state + add (mod 2^128)
+    RS_DEV void affine(u64 mlo, u64 mhi, u64 alo, u64 ahi) {
+        u64 plo = slo * mlo;
+        u64 phi = __umul64hi(slo, mlo) + slo * mhi + shi * mlo;
+        u64 r = plo + alo;
+        phi += ahi + (r < plo ? 1ULL : 0ULL);
+        slo = r; shi = phi;
+    }
+};
+
+RS_DEV void philox4x64_10(u64 c0, u64 c1, u64 c2, u64 c3, u64 k0, u64 k1, u64 &o0, u64 &o1, u64 &o2, u64 &o3) {
+    // counter.py:83-96
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+        u64 hi0 = __umul64hi(0xD2E7470EE14C6C93ULL, c0), lo0 = 0xD2E7470EE14C6C93ULL * c0;
+        u64 hi1 = __umul64hi(0xCA5A826395121157ULL, c2), lo1 = 0xCA5A826395121157ULL * c2;
+        u64 n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        k0 += 0x9E3779B97F4A7C15ULL;
+        k1 += 0xBB67AE8584CAA73BULL;
+    }
+    o0 = c0; o1 = c1; o2 = c2; o3 = c3;
+}
+
+struct EngPhilox {  // counter.py:98-121; words of a block are served x0..x3
+    u64 c0, c1, c2, c3, k0, k1;
+    u64 b0, b1, b2, b3;
+    int left;
+    RS_DEV void bump() {
+        c0 += 1;
+        if (c0 == 0) { c1 += 1; if (c1 == 0) { c2 += 1; if (c2 == 0) c3 += 1; } }
+    }
+    RS_DEV void add(u64 blocks) {
+        u64 o = c0;
+        c0 += blocks;
+        if (c0 < o) { c1 += 1; if (c1 == 0) { c2 += 1; if (c2 == 0) c3 += 1; } }
+    }
+    RS_DEV u64 next() {
+        if (left == 0) {
+            philox4x64_10(c0, c1, c2, c3, k0, k1, b0, b1, b2, b3);
+            bump();
+            left = 4;
+        }
+        u64 r = b0;
+        b0 = b1; b1 = b2; b2 = b3;
+        left--;
+        return r;
+    }
+};
+
+struct EngSfc {  // sfc.py:25-36
+    u64 a, b, c, w;
+    RS_DEV u64 next() {
+        u64 r = a + b + w;
+        w += 1;
+        a = b ^ (b >> 11);
+        b = c + (c << 3);
+        c = rotl64(c, 24) + r;
+        return r;
+    }
+};
+
+// ranlux++: x <- x*A mod m, m = 2^576 - 2^240 + 1 (ranlux.py:36-61); any exact
+// reduction yields the same canonical residue.
+RS_DEV void rlx_mulmod_dev(const u64 *x, const u64 *y, u64 *out) {
+    u64 p[18];
+#pragma unroll
+    for (int i = 0; i < 18; i++) p[i] = 0;
+#pragma unroll
+    for (int i = 0; i < 9; i++) {
+        u64 carry = 0;
+#pragma unroll
+        for (int j = 0; j < 9; j++) {
+            u64 lo = x[i] * y[j], hi = __umul64hi(x[i], y[j]);
+            u64 s = p[i + j] + lo;
+            hi += (s < lo) ? 1ULL : 0ULL;
+            u64 s2 = s + carry;
+            hi += (s2 < s) ? 1ULL : 0ULL;
+            p[i + j] = s2;
+            carry = hi;
+        }
+        p[i + 9] = carry;
+    }
+    // r = lo + (hi << 240) - hi over 13 limbs (>= 0)
+    u64 r[13];
+    {
+        u64 ca = 0, br = 0;
+#pragma unroll
+        for (int i = 0; i < 13; i++) {
+            u64 a = i < 9 ? p[i] : 0ULL;
+            u64 sh = 0;
+            if (i >= 3 && i - 3 < 9) sh |= p[9 + i - 3] << 48;
+            if (i >= 4 && i - 4 < 9) sh |= p[9 + i - 4] >> 16;
+            u64 t = a + sh;
+            u64 c1 = t < a ? 1ULL : 0ULL;
+            u64 t2 = t + ca;
+            c1 += t2 < t ? 1ULL : 0ULL;
+            ca = c1;
+            u64 h = i < 9 ? p[9 + i] : 0ULL;
+            u64 d = t2 - h;
+            u64 b1 = t2 < h ? 1ULL : 0ULL;
+            u64 d2 = d - br;
+            b1 += d < br ? 1ULL : 0ULL;
+            br = b1;
+            r[i] = d2;
+        }
+    }
+    // fold r[9..12] again into 10 limbs
+    u64 q[10];
+    {
+        u64 ca = 0, br = 0;
+#pragma unroll
+        for (int i = 0; i < 10; i++) {
+            u64 a = i < 9 ? r[i] : 0ULL;
+            u64 sh = 0;
+            if (i >= 3 && i - 3 < 4) sh |= r[9 + i - 3] << 48;
+            if (i >= 4 && i - 4 < 4) sh |= r[9 + i - 4] >> 16;
+            u64 t = a + sh;
+            u64 c1 = t < a ? 1ULL : 0ULL;
+            u64 t2 = t + ca;
+            c1 += t2 < t ? 1ULL : 0ULL;
+            ca = c1;
+            u64 h = i < 4 ? r[9 + i] : 0ULL;
+            u64 d = t2 - h;
+            u64 b1 = t2 < h ? 1ULL : 0ULL;
+            u64 d2 = d - br;
+            b1 += d < br ? 1ULL : 0ULL;
+            br = b1;
+            q[i] = d2;
+        }
+    }
+    // q < 2m: one conditional subtraction of m
+    const u64 M[9] = {1ULL, 0ULL, 0ULL, 0xFFFF000000000000ULL, ~0ULL, ~0ULL, ~0ULL, ~0ULL, ~0ULL};
+    bool ge = q[9] != 0;
+    if (!ge) {
+        ge = true;
+        bool decided = false;
+#pragma unroll
+        for (int i = 8; i >= 0; i--) {
+            if (!decided && q[i] != M[i]) { ge = q[i] > M[i]; decided = true; }
+        }
+    }
+    if (ge) {
+        u64 br = 0;
+#pragma unroll
+        for (int i = 0; i < 9; i++) {
+            u64 d = q[i] - M[i];
+            u64 b1 = q[i] < M[i] ? 1ULL : 0ULL;
+            u64 d2 = d - br;
+            b1 += d < br ? 1ULL : 0ULL;
+            br = b1;
+            q[i] = d2;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 9; i++) out[i] = q[i];
+}
+
+struct EngRanlux {  // words of a chunk: the 9 limbs of the new residue, low first
+    u64 x[9];
+    u64 o[9];
+    int left;
+    const u64 *A;  // multiplier limbs (global)
+    RS_DEV u64 next() {
+        if (left == 0) {
+            u64 a[9];
+#pragma unroll
+            for (int i = 0; i < 9; i++) a[i] = __ldg(A + i);
+            rlx_mulmod_dev(x, a, x);
+#pragma unroll
+            for (int i = 0; i < 9; i++) o[i] = x[i];
+            left = 9;
+        }
+        u64 r = o[0];
+#pragma unroll
+        for (int i = 0; i < 8; i++) o[i] = o[i + 1];
+        left--;
+        return r;
+    }
+};
+
+// ----------------------------------------------------------------------------- uniforms
+RS_DEV double dbl(u64 b) { return __longlong_as_double((long long)b); }
+RS_DEV u64 bits(double d) { return (u64)__double_as_longlong(d); }
+
+// Rng.u01, rng.py:98-106
+RS_DEV double u01_of(u64 w, bool fm) {
+    if (fm) return (double)(w >> 11) * 1.1102230246251565e-16;
+    return dbl((w >> 12) | 0x3FF0000000000000ULL) - 1.0;
+}
+// Rng.u01f on one u32 half, rng.py:108-115 (exact in f32 either way)
+RS_DEV float u01f_of(u32 h, bool fm) {
+    if (fm) return (float)((double)(h >> 8) * 5.9604644775390625e-08);
+    return (float)((double)__uint_as_float((h >> 9) | 0x3F800000u) - 1.0);
+}
+
+// ----------------------------------------------------------------------------- detmath
+RS_DEV u32 hiw(double x) { return (u32)(bits(x) >> 32); }
+RS_DEV double with_hiw(double x, u32 h) { return dbl(((u64)h << 32) | (bits(x) & 0xFFFFFFFFULL)); }
+
+// det_exp, detmath.py:59-104
+__device__ __noinline__ double det_exp_dev(double x) {
+    const double huge = 1.0e300, twom1000 = 9.33263618503218878990e-302;
+    const double o_thr = 7.09782712893383973096e+02, u_thr = -7.45133219101941108420e+02;
+    const double invln2 = 1.44269504088896338700e+00, ln2hi = 6.93147180369123816490e-01,
+                 ln2lo = 1.90821492927058770002e-10;
+    const double P1 = 1.66666666666666019037e-01, P2 = -2.77777777770155933842e-03,
+                 P3 = 6.61375632143793436117e-05, P4 = -1.65339022054652515390e-06,
+                 P5 = 4.13813679705723846039e-08;
+    u32 hx = hiw(x);
+    int xsb = (hx >> 31) & 1;
+    hx &= 0x7FFFFFFFu;
+    if (hx >= 0x40862E42u) {
+        if (hx >= 0x7FF00000u) {
+            if (((hx & 0xFFFFFu) | (u32)bits(x)) != 0) return x + x;
+            return xsb == 0 ? x : 0.0;
+        }
+        if (x > o_thr) return huge * huge;
+        if (x < u_thr) return twom1000 * twom1000;  // underflow to +0 (fdlibm)
+    }
+    int k = 0;
+    double hi = 0.0, lo = 0.0;
+    if (hx > 0x3FD62E42u) {
+        if (hx < 0x3FF0A2E4u) {
+            if (xsb == 0) { hi = x - ln2hi; lo = ln2lo; k = 1; }
+            else { hi = x + ln2hi; lo = -ln2lo; k = -1; }
+        } else {
+            double kd = invln2 * x + (xsb == 0 ? 0.5 : -0.5);
+            k = __double2int_rz(kd);  // Python int(): truncation toward zero
+            double t = (double)k;
+            hi = x - t * ln2hi;
+            lo = t * ln2lo;
+        }
+        x = hi - lo;
+    } else if (hx < 0x3E300000u) {
+        if (huge + x > 1.0) return 1.0 + x;
+    }
+    double t = x * x;
+    double c = x - t * (P1 + t * (P2 + t * (P3 + t * (P4 + t * P5))));
+    if (k == 0) return 1.0 - ((x * c / (c - 2.0)) - x);
+    double y = 1.0 - ((lo - (x * c) / (2.0 - c)) - hi);
+    if (k >= -1021) return with_hiw(y, hiw(y) + ((u32)k << 20));
+    return with_hiw(y, hiw(y) + ((u32)(k + 1000) << 20)) * twom1000;
+}
+
+// det_log, detmath.py:107-163
+__device__ __noinline__ double det_log_dev(double x) {
+    const double ln2hi = 6.93147180369123816490e-01, ln2lo = 1.90821492927058770002e-10;
+    const double two54 = 1.80143985094819840000e+16;
+    const double Lg1 = 6.666666666666735130e-01, Lg2 = 3.999999999940941908e-01,
+                 Lg3 = 2.857142874366239149e-01, Lg4 = 2.222219843214978396e-01,
+                 Lg5 = 1.818357216161805012e-01, Lg6 = 1.531383769920937332e-01,
+                 Lg7 = 1.479819860511658591e-01;
+    u64 u = bits(x);
+    int hx = (int)(u >> 32);
+    u32 lx = (u32)u;
+    int k = 0;
+    if (hx < 0) {
+        if (((hx & 0x7FFFFFFF) | (int)lx) == 0) return dbl(0xFFF0000000000000ULL);  // -inf
+        return dbl(0x7FF8000000000000ULL);                                          // nan
+    }
+    if (hx < 0x00100000) {
+        if ((hx | (int)lx) == 0) return dbl(0xFFF0000000000000ULL);
+        k -= 54;
+        x *= two54;
+        hx = (int)hiw(x);
+    }
+    if (hx >= 0x7FF00000) return x + x;
+    k += (hx >> 20) - 1023;
+    hx &= 0x000FFFFF;
+    int i = (hx + 0x95F64) & 0x100000;
+    x = with_hiw(x, (u32)(hx | (i ^ 0x3FF00000)));
+    k += i >> 20;
+    double f = x - 1.0;
+    if ((0x000FFFFF & (2 + hx)) < 3) {
+        if (f == 0.0) {
+            if (k == 0) return 0.0;
+            double dk = (double)k;
+            return dk * ln2hi + dk * ln2lo;
+        }
+        double R = f * f * (0.5 - 0.33333333333333333 * f);
+        if (k == 0) return f - R;
+        double dk = (double)k;
+        return dk * ln2hi - ((R - dk * ln2lo) - f);
+    }
+    double s = f / (2.0 + f);
+    double dk = (double)k;
+    double z = s * s;
+    int ii = hx - 0x6147A;
+    double w = z * z;
+    int j = 0x6B851 - hx;
+    double t1 = w * (Lg2 + w * (Lg4 + w * Lg6));
+    double t2 = z * (Lg1 + w * (Lg3 + w * (Lg5 + w * Lg7)));
+    ii |= j;
+    double R = t2 + t1;
+    if (ii > 0) {
+        double hfsq = 0.5 * f * f;
+        if (k == 0) return f - (hfsq - s * (hfsq + R));
+        return dk * ln2hi - ((hfsq - (s * (hfsq + R) + dk * ln2lo)) - f);
+    }
+    if (k == 0) return f - s * (f - R);
+    return dk * ln2hi - ((s * (f - R) - dk * ln2lo) - f);
+}
+
+// ----------------------------------------------------------------------------- parsers
+
+// The fast-path strip {K, W} (16 B) lives in shared memory; slow-path data in global.
+struct ZigFast {
+    u64 k;
+    double w;
+};
+
+RS_DEV bool lt128(u64 alo, u64 ahi, u64 blo, u64 bhi) { return ahi < bhi || (ahi == bhi && alo < blo); }
+
+// lhs = yv*d + (rabs-K)*2^52 exactly (continuous.py:59-61)
+RS_DEV void zig_lhs(u64 yv, u64 d, u64 rk, u64 &lo, u64 &hi) {
+    u64 plo = yv * d, phi = __umul64hi(yv, d);
+    u64 slo = rk << 52, shi = rk >> 12;
+    lo = plo + slo;
+    hi = phi + shi + (lo < plo ? 1ULL : 0ULL);
+}
+
+// std_norm, continuous.py:40-68.  Tallies: norm attempts / pdf_evals of the
+// current (not yet emitted) sample.
+struct NormP {
+    const ZigFast *fast;  // smem, 256 strips
+    const RsZigSlow *slow;
+    bool fm;
+    int st;  // 0 start, 1 slow (second word), 2 tail xx, 3 tail yy
+    int idx;
+    u32 sign;
+    u64 rabs;
+    double x, xx;
+    u32 att, pdf;
+    RS_DEV void init(const ZigFast *f, const RsZigSlow *s, bool full_mantissa) {
+        fast = f; slow = s; fm = full_mantissa; st = 0; att = 0; pdf = 0;
+    }
+    // returns true when a sample is emitted into z
+    RS_DEV bool feed(u64 w, double &z) {
+        if (st == 0) {
+            att++;
+            idx = (int)(w & 0xFF);
+            sign = (u32)((w >> 8) & 1);
+            rabs = (w >> 9) & ((1ULL << 52) - 1);
+            ZigFast f = fast[idx];
+            x = (double)rabs * f.w;
+            if (rabs < f.k) { z = sign ? -x : x; return true; }
+            st = idx == 0 ? 2 : 1;
+            return false;
+        }
+        if (st == 1) {
+            st = 0;
+            u64 yv = w >> 12;
+            u64 K = __ldg(&slow->k[idx]);
+            u64 lo, hi;
+            zig_lhs(yv, (1ULL << 52) - K, rabs - K, lo, hi);
+            if (lt128(lo, hi, __ldg(&slow->ta_lo[idx]), __ldg(&slow->ta_hi[idx]))) { z = sign ? -x : x; return true; }
+            if (!lt128(__ldg(&slow->tr_lo[idx]), __ldg(&slow->tr_hi[idx]), lo, hi)) {
+                pdf++;
+                double fi = __ldg(&slow->f[idx]), fim1 = __ldg(&slow->f[idx - 1]);
+                double y = fi + ((double)yv * 2.220446049250313e-16) * (fim1 - fi);
+                if (y < det_exp_dev(-0.5 * x * x)) { z = sign ? -x : x; return true; }
+            }
+            return false;  // reject: a fresh attempt starts at the next word
+        }
+        if (st == 2) {
+            xx = -dbl(RS_NOR_INV_R_BITS) * det_log_dev(1.0 - u01_of(w, fm));
+            st = 3;
+            return false;
+        }
+        double yy = -det_log_dev(1.0 - u01_of(w, fm));
+        if (yy + yy > xx * xx) {
+            double t = dbl(RS_NOR_R_BITS) + xx;
+            z = sign ? -t : t;
+            st = 0;
+            return true;
+        }
+        st = 2;
+        return false;
+    }
+};
+
+// std_exp, continuous.py:71-93
+struct ExpP {
+    const ZigFast *fast;
+    const RsZigSlow *slow;
+    bool fm;
+    int st;
+    int idx;
+    u64 rabs;
+    double x;
+    u32 att, pdf;
+    RS_DEV void init(const ZigFast *f, const RsZigSlow *s, bool full_mantissa) {
+        fast = f; slow = s; fm = full_mantissa; st = 0; att = 0; pdf = 0;
+    }
+    RS_DEV bool feed(u64 w, double &z) {
+        if (st == 0) {
+            att++;
+            idx = (int)(w & 0xFF);
+            rabs = (w >> 8) & ((1ULL << 53) - 1);
+            ZigFast f = fast[idx];
+            x = (double)rabs * f.w;
+            if (rabs < f.k) { z = x; return true; }
+            st = idx == 0 ? 2 : 1;
+            return false;
+        }
+        if (st == 1) {
+            st = 0;
+            u64 yv = w >> 12;
+            u64 K = __ldg(&slow->k[idx]);
+            u64 lo, hi;
+            zig_lhs(yv, (1ULL << 53) - K, rabs - K, lo, hi);
+            if (lt128(lo, hi, __ldg(&slow->ta_lo[idx]), __ldg(&slow->ta_hi[idx]))) { z = x; return true; }
+            if (!lt128(__ldg(&slow->tr_lo[idx]), __ldg(&slow->tr_hi[idx]), lo, hi)) {
+                pdf++;
+                double fe = __ldg(&slow->f[idx]), fem1 = __ldg(&slow->f[idx - 1]);
+                double y = fe + ((double)yv * 2.220446049250313e-16) * (fem1 - fe);
+                if (y < det_exp_dev(-x)) { z = x; return true; }
+            }
+            return false;
+        }
+        z = dbl(RS_EXP_R_BITS) - det_log_dev(1.0 - u01_of(w, fm));
+        st = 0;
+        return true;
+    }
+};
+
+// Marsaglia-Tsang gamma with the power-of-uniform boost below 1, continuous.py:183-212.
+struct GammaPrm {
+    double d, cc, td;   // d = a-1/3, cc = 1/sqrt(9d), td = theta*d (alpha >= 1 core)
+    double alpha, theta;
+    int boost;          // alpha < 1: core runs gamma(alpha+1, 1)
+};
+struct GammaP {
+    NormP np;
+    GammaPrm g;
+    int st;        // 0 need z (normal sub-parser), 1 need u, 2 need boost u
+    bool fresh;    // next z-word starts a new attempt
+    double z, v, base;
+    u32 gatt;
+    RS_DEV void init(const ZigFast *f, const RsZigSlow *s, bool fm, const GammaPrm &p) {
+        np.init(f, s, fm);
+        g = p; st = 0; fresh = true; gatt = 0;
+    }
+    RS_DEV bool feed(u64 w, double &out) {
+        if (st == 0) {
+            if (fresh) { gatt++; fresh = false; }
+            double zz0;
+            if (np.feed(w, zz0)) {
+                double t = 1.0 + g.cc * zz0;
+                if (t > 0.0) { z = zz0; v = t * t * t; st = 1; }
+            }
+            return false;
+        }
+        if (st == 1) {
+            double u = u01_of(w, np.fm);
+            double zz = z * z;
+            bool acc = u < 1.0 - 0.0331 * zz * zz;
+            if (!acc) acc = det_log_dev(u) < 0.5 * zz + g.d - g.d * v + g.d * det_log_dev(v);
+            st = 0;
+            fresh = true;
+            if (!acc) return false;
+            double r = g.td * v;
+            if (!g.boost) { out = r; return true; }
+            base = r;
+            st = 2;
+            return false;
+        }
+        // boost: theta * base * det_exp(det_log(u) / alpha)
+        double u = u01_of(w, np.fm);
+        out = g.theta * base * det_exp_dev(det_log_dev(u) / g.alpha);
+        st = 0;
+        return true;
+    }
+};
+
+// ----------------------------------------------------------------------------- distributions
+// A Dist turns the word stream into samples: feed(w, out) returns true on an
+// emission; tally(t6) moves the finished sample's diagnostics into t6[6].
+
+struct DistStdNorm {
+    typedef double out_t;
+    NormP p;
+    RS_DEV bool feed(u64 w, double &o) { return p.feed(w, o); }
+    RS_DEV void tally(u64 *t) { t[0] += p.att; t[1] += p.pdf; p.att = 0; p.pdf = 0; }
+    RS_DEV void drop() { p.att = 0; p.pdf = 0; }
+};
+struct DistNorm {  // norm epilogue: float(mu) + sqrt(var) * z (continuous.py:157-158)
+    typedef double out_t;
+    NormP p;
+    double mu, sd;
+    RS_DEV bool feed(u64 w, double &o) {
+        double z;
+        if (!p.feed(w, z)) return false;
+        o = mu + sd * z;
+        return true;
+    }
+    RS_DEV void tally(u64 *t) { t[0] += p.att; t[1] += p.pdf; p.att = 0; p.pdf = 0; }
+    RS_DEV void drop() { p.att = 0; p.pdf = 0; }
+};
+struct DistExp {  // beta * std_exp (continuous.py:165-169)
+    typedef double out_t;
+    ExpP p;
+    double beta;
+    RS_DEV bool feed(u64 w, double &o) {
+        double x;
+        if (!p.feed(w, x)) return false;
+        o = beta * x;
+        return true;
+    }
+    RS_DEV void tally(u64 *t) { t[2] += p.att; t[3] += p.pdf; p.att = 0; p.pdf = 0; }
+    RS_DEV void drop() { p.att = 0; p.pdf = 0; }
+};
+struct DistGamma {
+    typedef double out_t;
+    GammaP p;
+    RS_DEV bool feed(u64 w, double &o) { return p.feed(w, o); }
+    RS_DEV void tally(u64 *t) {
+        t[0] += p.np.att; t[1] += p.np.pdf; t[4] += p.gatt;
+        p.np.att = 0; p.np.pdf = 0; p.gatt = 0;
+    }
+    RS_DEV void drop() { p.np.att = 0; p.np.pdf = 0; p.gatt = 0; }
+};
+struct DistBeta {  // x = gamma(a,1) then y = gamma(b,1); x/(x+y) (continuous.py:215-218)
+    typedef double out_t;
+    GammaP p;
+    GammaPrm ga, gb;
+    int phase;
+    double xa;
+    RS_DEV bool feed(u64 w, double &o) {
+        double r;
+        if (!p.feed(w, r)) return false;
+        if (phase == 0) {
+            xa = r; phase = 1; p.g = gb;
+            return false;
+        }
+        o = xa / (xa + r);
+        phase = 0; p.g = ga;
+        return true;
+    }
+    RS_DEV void tally(u64 *t) {
+        t[0] += p.np.att; t[1] += p.np.pdf; t[4] += p.gatt;
+        p.np.att = 0; p.np.pdf = 0; p.gatt = 0;
+    }
+    RS_DEV void drop() { p.np.att = 0; p.np.pdf = 0; p.gatt = 0; }
+};
+struct DistLemire {  // bounded_uint(rng, b, 64), discrete.py:20-39: accept iff low >= (2^64-b) % b
+    typedef u64 out_t;
+    u64 b, thr;
+    RS_DEV bool feed(u64 w, u64 &o) {
+        u64 low = w * b;
+        if (low < thr) return false;
+        o = __umul64hi(w, b);
+        return true;
+    }
+    RS_DEV void tally(u64 *) {}
+    RS_DEV void drop() {}
+};
+struct DistRaw {
+    typedef u64 out_t;
+    RS_DEV bool feed(u64 w, u64 &o) { o = w; return true; }
+    RS_DEV void tally(u64 *) {}
+    RS_DEV void drop() {}
+};
+struct DistU01 {
+    typedef double out_t;
+    bool fm;
+    RS_DEV bool feed(u64 w, double &o) { o = u01_of(w, fm); return true; }
+    RS_DEV void tally(u64 *) {}
+    RS_DEV void drop() {}
+};
+
+// ----------------------------------------------------------------------------- 256-bit writer
+// Writes a contiguous run of 8-byte elements starting at element `start` of
+// `out`; full 32-byte-aligned groups go out as one STG.256, the ragged head and
+// tail as scalar stores.
+template <class T>
+struct VecWriter8 {
+    T *abase;      // 32-byte aligned base
+    u64 vi;        // element index (from abase) of the current group
+    int slot, first;
+    T v0, v1, v2, v3;
+    RS_DEV void init(T *out, u64 start) {
+        uintptr_t a = (uintptr_t)out;
+        abase = (T *)(a & ~(uintptr_t)31);
+        u64 s = start + ((a & 31) >> 3);
+        vi = s & ~3ULL;
+        slot = (int)(s & 3);
+        first = slot;
+    }
+    RS_DEV void put(T v) {
+        switch (slot) {
+        case 0: v0 = v; break;
+        case 1: v1 = v; break;
+        case 2: v2 = v; break;
+        default: v3 = v; break;
+        }
+        if (++slot == 4) flush_full();
+    }
+    RS_DEV void flush_full() {
+        T *p = abase + vi;
+        if (first == 0) {
+            u64 a = *(u64 *)&v0, b = *(u64 *)&v1, c = *(u64 *)&v2, d = *(u64 *)&v3;
+            asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d)
+                         : "memory");
+        } else {
+            if (first <= 1) p[1] = v1;
+            if (first <= 2) p[2] = v2;
+            p[3] = v3;
+        }
+        first = 0;
+        slot = 0;
+        vi += 4;
+    }
+    RS_DEV void finish() {
+        T *p = abase + vi;
+        if (first == 0 && slot > 0) p[0] = v0;
+        if (first <= 1 && slot > 1) p[1] = v1;
+        if (first <= 2 && slot > 2) p[2] = v2;
+    }
+};

@@ -1,0 +1,462 @@
+"""The generator facade: drop-in for the reference's `Rng` (pkg/src/randstream/rng.py).
+
+Same surface and semantics -- word primitives, uniforms, seed / randomize /
+jump / advance / set_stream, state, modes, duplicate, fill, mvn, the
+per-instance error slot -- with one difference in *where* work runs:
+`fill` and `mvn` (the bulk hot path, rng.py:223-241 / 273-275) always run on
+the GPU through the C ABI (`rs_fill`, `rs_mvn`) and return device tensors.
+Scalar word primitives (next_u64 / next_u32 / u01 / u01f / raw) consume the
+host-side 144-word buffer exactly as the reference does; the scalar sampler
+conveniences (norm, expo, gamma, unif, bounded_uint) are one-element device
+fills. After any fill the engine state and buffer equal the reference's
+(SURVEY 8(b)), so scalar draws, duplicate() and to_blob() continue bit-exactly.
+"""
+
+import ctypes
+import math
+from functools import wraps
+from struct import pack, unpack
+
+import numpy as np
+import torch
+
+from . import _lib, engines, seeding
+from .buffer import CAPACITY, WordBuffer
+
+MASK64 = 0xFFFFFFFFFFFFFFFF
+
+_POLY_JUMP = {"x256++", "x256**"}
+STANDARD_JUMPS = (32, 64, 96, 128, 192)  # jumps.py:24
+_STREAM_METHODS = {  # rng.py:27-35
+    "pcg64": ("set_inc", 2),
+    "squares": ("set_key", 1),
+    "philox": ("set_key", 2),
+    "sfc64": ("set_abc", 3),
+    "sfc64simd": ("set_abc", 3),
+    "cwg128": ("set_weyl", 2),
+    "chacha20": ("set_nonce", 2),
+}
+
+# the reference's continuous + discrete names (continuous.py:339-359, discrete.py:95-100)
+SCALAR_NAMES = ("u01", "u01f", "unif", "uniff", "norm", "normf", "exp", "expf", "lognormal", "gamma", "beta",
+                "chi2", "t", "f", "gumbel", "pareto", "gpd", "weibull", "skew_normal")
+DISCRETE_NAMES = ("uint8", "uint16", "uint32", "uint64", "int", "long_long")
+DEVICE_DISTS = ("u01", "u01f", "norm", "exp", "gamma", "beta", "uint64")
+
+# accepted keyword parameters of each device sampler: (allowed, required) -- continuous.py signatures
+_SIGNATURES = {
+    "u01": ((), ()),
+    "u01f": ((), ()),
+    "norm": (("mu", "var"), ()),
+    "exp": (("beta",), ()),
+    "gamma": (("alpha", "theta"), ("alpha",)),
+    "beta": (("a", "b"), ("a", "b")),
+}
+_TALLY_NAMES = ("norm", "exp", "gamma")
+
+
+def _op(fn):
+    """Per-instance error slot (rng.py:38-52): success clears, failure records."""
+
+    @wraps(fn)
+    def guarded(self, *args, **kwargs):
+        try:
+            result = fn(self, *args, **kwargs)
+        except Exception as exc:
+            self.last_error = str(exc) or type(exc).__name__
+            raise
+        self.last_error = None
+        return result
+
+    return guarded
+
+
+def _cuda_stream_ptr(device):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _out_dtype(dist):
+    if dist == "uint64":
+        return torch.uint64
+    if dist == "u01f":
+        return torch.float32
+    return torch.float64
+
+
+class Rng:
+    def __init__(self, engine):
+        self.engine = engine
+        self.buffer = WordBuffer(engine)
+        self.bitexact = False
+        self.full_mantissa = False
+        self.counters = {}
+        self.last_error = None
+        self.entropy_source = None
+        self.entropy_degraded = False
+        self.device = None  # torch device for fills (default: current CUDA device)
+
+    @property
+    def engine_id(self):
+        return self.engine.ID
+
+    # ---------------------------------------------------------------- word primitives (host)
+    @_op
+    def next_u64(self):
+        return self.buffer.take_u64()
+
+    @_op
+    def next_u32(self):
+        return self.buffer.take_u32()
+
+    @_op
+    def raw(self, nbytes):
+        """rng.py:80-94: little-endian bytes; a trailing partial word is truncated."""
+        nbytes = int(nbytes)
+        if nbytes < 0:
+            raise ValueError("byte count must be >= 0")
+        full, rest = divmod(nbytes, 8)
+        out = bytearray()
+        for _ in range(full):
+            out += pack("<Q", self.buffer.take_u64())
+        if rest:
+            out += pack("<Q", self.buffer.take_u64())[:rest]
+        return bytes(out)
+
+    @_op
+    def u01(self):
+        w = self.buffer.take_u64()
+        if self.full_mantissa:
+            return (w >> 11) * 1.1102230246251565e-16
+        return unpack("<d", pack("<Q", (w >> 12) | 0x3FF0000000000000))[0] - 1.0
+
+    @_op
+    def u01f(self):
+        w = self.buffer.take_u32()
+        if self.full_mantissa:
+            return (w >> 8) * 5.9604644775390625e-08
+        return float(unpack("<f", pack("<I", (w >> 9) | 0x3F800000))[0]) - 1.0
+
+    # ---------------------------------------------------------------- seeding / streams
+    @_op
+    def seed(self, entropy_words, spawn_key=()):
+        seeding.seed_engine(self.engine, entropy_words, spawn_key)
+        self.buffer.reset()
+        self.entropy_source = "seed"
+        self.entropy_degraded = False
+
+    @_op
+    def randomize(self):
+        words, source, degraded = seeding.random_entropy()
+        seeding.seed_engine(self.engine, words)
+        self.buffer.reset()
+        self.entropy_source = source
+        self.entropy_degraded = degraded
+        return source, degraded
+
+    @_op
+    def jump(self, k):
+        """rng.py:135-164: x256 family 2^k steps (k in the committed table), pcg64
+        advance(2^k), ranlux++ x*A^(2^k); others raise."""
+        k = int(k)
+        eid = self.engine_id
+        if eid in _POLY_JUMP:
+            if k not in STANDARD_JUMPS + (253,):
+                raise ValueError("no jump polynomial for family 'x256' at 2^%d" % k)
+        elif eid in ("pcg64", "ranlux++"):
+            if k not in STANDARD_JUMPS:
+                raise ValueError("%s jump exponent must be one of %s" % (eid, STANDARD_JUMPS))
+        else:
+            raise ValueError("jump unsupported for engine %s" % eid)
+        st = _lib.u64_array(self.engine.s, 9)
+        _lib.check(_lib.lib.rs_engine_jump(self.engine.native, st, k))
+        self.engine.s = [int(st[i]) for i in range(self.engine.STATE_WORDS)]
+        self.buffer.reset()
+
+    @_op
+    def advance(self, delta):
+        if self.engine_id != "pcg64":
+            raise ValueError("advance unsupported for engine %s" % self.engine_id)
+        d = int(delta) & ((1 << 128) - 1)
+        st = _lib.u64_array(self.engine.s, 9)
+        _lib.check(_lib.lib.rs_pcg_advance(st, d & MASK64, d >> 64))
+        self.engine.s = [int(st[i]) for i in range(4)]
+        self.buffer.reset()
+
+    @_op
+    def set_stream(self, words):
+        eid = self.engine_id
+        if eid not in _STREAM_METHODS:
+            raise ValueError("stream selection unsupported for engine %s; use jumps or spawn keys" % eid)
+        method, nwords = _STREAM_METHODS[eid]
+        if len(words) != nwords:
+            raise ValueError("%s stream selector takes %d words, got %d" % (eid, nwords, len(words)))
+        getattr(self.engine, method)([int(w) & MASK64 for w in words])
+        self.buffer.reset()
+
+    # ---------------------------------------------------------------- state / modes
+    @_op
+    def get_state(self):
+        return self.engine.get_state()
+
+    @_op
+    def set_state(self, words):
+        self.engine.set_state(words)
+        self.buffer.reset()
+
+    @_op
+    def set_bitexact(self, flag):
+        self.bitexact = bool(flag)
+
+    @_op
+    def set_full_mantissa(self, flag):
+        self.full_mantissa = bool(flag)
+
+    @_op
+    def duplicate(self):
+        other = Rng(engines.make(self.engine_id))
+        other.engine.s = list(self.engine.s)
+        other.buffer.restore(self.buffer.capture())
+        other.bitexact = self.bitexact
+        other.full_mantissa = self.full_mantissa
+        other.counters = {k: dict(v) for k, v in self.counters.items()}
+        other.device = self.device
+        return other
+
+    # ---------------------------------------------------------------- device boundary
+    def to_stream(self):
+        """The generator's logical position as an rs_stream (C ABI struct)."""
+        s = _lib.RsStream()
+        s.engine = self.engine.native
+        s.full_mantissa = int(self.full_mantissa)
+        s.bitexact = int(self.bitexact)
+        s.has_pending = 0 if self.buffer.pending is None else 1
+        s.pending = self.buffer.pending or 0
+        for i, w in enumerate(self.engine.s):
+            s.state[i] = w
+        words = self.buffer.words
+        for i, w in enumerate(words):
+            s.buf[i] = w
+        s.fill = len(words)
+        s.cursor = self.buffer.cursor
+        return s
+
+    def from_stream(self, s):
+        self.engine.s = [int(s.state[i]) for i in range(self.engine.STATE_WORDS)]
+        self.buffer.words = [int(s.buf[i]) for i in range(s.fill)]
+        self.buffer.cursor = int(s.cursor)
+        self.buffer.pending = int(s.pending) if s.has_pending else None
+
+    def _device(self):
+        if self.device is not None:
+            return torch.device(self.device)
+        if not torch.cuda.is_available():
+            raise _lib.LibraryError("no CUDA device: the fill path runs only on the GPU")
+        return torch.device("cuda", torch.cuda.current_device())
+
+    def _add_tallies(self, res):
+        for i, name in enumerate(_TALLY_NAMES):
+            if res.tally_seen[i]:
+                c = self.counters.setdefault(name, {"attempts": 0, "pdf_evals": 0})
+                c["attempts"] += int(res.tally[2 * i])
+                c["pdf_evals"] += int(res.tally[2 * i + 1])
+
+    def device_fill(self, dist, fparams, iparams, n, out=None):
+        """Run rs_fill for `n` samples of a validated device distribution."""
+        n = int(n)
+        if n == 0 and out is None:  # nothing is consumed (continuous.py:422-427 runs zero times)
+            dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else "cpu"
+            return torch.empty(0, dtype=_out_dtype(dist), device=dev)
+        if out is None:
+            dev = self._device()
+            out = torch.empty(n, dtype=_out_dtype(dist), device=dev)
+        if isinstance(out, torch.Tensor):
+            if out.numel() < n or not out.is_contiguous():
+                raise ValueError("out must be a contiguous tensor with at least n elements")
+            ptr = out.data_ptr()
+            stream = _cuda_stream_ptr(out.device) if out.is_cuda else ctypes.c_void_p(0)
+        else:  # numpy host array (the e2e path: the library stages through device memory)
+            arr = out
+            if arr.size < n or not arr.flags["C_CONTIGUOUS"]:
+                raise ValueError("out must be a contiguous array with at least n elements")
+            ptr = arr.ctypes.data
+            stream = _cuda_stream_ptr(self._device())
+        st = self.to_stream()
+        res = _lib.RsFillResult()
+        fp = (ctypes.c_double * 4)(*(list(fparams) + [0.0] * (4 - len(fparams))))
+        ip = _lib.u64_array(list(iparams), 4)
+        _lib.check(_lib.lib.rs_fill(ctypes.byref(st), _lib.DIST_IDS[dist], fp, ip, n, ctypes.c_void_p(ptr),
+                                    ctypes.byref(res), stream))
+        self.from_stream(st)
+        self._add_tallies(res)
+        self.last_fill = res
+        return out
+
+    # ---------------------------------------------------------------- fill (the hot path)
+    @_op
+    def fill(self, dist, params=None, n=1, out=None):
+        """n draws of a named distribution on the GPU (rng.py:223-241).
+
+        Returns a 1-D device tensor (uint64 / float64 / float32 for u01f);
+        `.tolist()` gives the reference's list. `out` may be a device tensor or a
+        host numpy array (staged through device memory by the library)."""
+        params = dict(params or {})
+        if dist in ("perm", "sample"):
+            raise NotImplementedError("%s draws are sequences, not bulk fills; not on the B200 fill path" % dist)
+        if dist in SCALAR_NAMES:
+            n = int(n)
+            if n < 0:
+                raise ValueError("draw count must be >= 0")
+            if dist not in DEVICE_DISTS:
+                raise NotImplementedError("distribution %r is not on the B200 fill path yet" % dist)
+            fp = self._continuous_params(dist, params, n)
+            return self.device_fill(dist, fp, [], n, out)
+        n = int(n)
+        if n < 0:
+            raise ValueError("draw count must be >= 0")
+        if dist in DISCRETE_NAMES:
+            if dist != "uint64":
+                raise NotImplementedError("distribution %r is not on the B200 fill path yet" % dist)
+            b = int(params.get("b", 0))
+            if n > 0 and (b < 0 or b > (1 << 64)):
+                raise ValueError("bound must be in [0, 2^64]")
+            ip = [0, 1] if b == 1 << 64 else [b, 0]
+            return self.device_fill("uint64", [], ip, n, out)
+        raise ValueError("unknown discrete distribution %r" % dist)
+
+    def _continuous_params(self, dist, params, n):
+        """Reference validation order (continuous.py:413-431 + sampler bodies):
+        nothing is checked for n == 0; otherwise bad keywords -> 'bad parameters',
+        then the sampler's own value checks, before any word is consumed."""
+        if n == 0:
+            return [0.0, 0.0]
+        allowed, required = _SIGNATURES[dist]
+        if any(k not in allowed for k in params) or any(k not in params for k in required):
+            raise ValueError("bad parameters for %s: %r" % (dist, sorted(params)))
+        if dist == "norm":
+            mu = float(params.get("mu", 0.0))
+            var = float(params.get("var", 1.0))
+            if not var >= 0.0:
+                raise ValueError("normal variance must be >= 0")
+            return [mu, var]
+        if dist == "exp":
+            beta = float(params.get("beta", 1.0))
+            if not beta > 0.0:
+                raise ValueError("exponential scale must be > 0")
+            return [beta]
+        if dist == "gamma":
+            alpha, theta = float(params["alpha"]), float(params.get("theta", 1.0))
+            if not alpha > 0.0:
+                raise ValueError("gamma shape must be > 0")
+            if not theta > 0.0:
+                raise ValueError("gamma scale must be > 0")
+            return [alpha, theta]
+        if dist == "beta":
+            a, b = float(params["a"]), float(params["b"])
+            if not a > 0.0:
+                raise ValueError("gamma shape must be > 0")
+            if not b > 0.0:
+                # beta draws gamma(a) before gamma(b) raises (continuous.py:215-218):
+                # consume exactly that one gamma(a) sample, then fail.
+                self.device_fill("gamma", [a, 1.0], [], 1)
+                raise ValueError("gamma shape must be > 0")
+            return [a, b]
+        return []
+
+    # ---------------------------------------------------------------- scalar conveniences
+    @_op
+    def unif(self, a=0.0, b=1.0):
+        a, b = float(a), float(b)
+        if not b > a:
+            raise ValueError("unif needs b > a")
+        return a + self.u01() * (b - a)
+
+    @_op
+    def norm(self, mu=0.0, var=1.0):
+        return float(self.fill("norm", {"mu": mu, "var": var}, 1)[0].item())
+
+    @_op
+    def expo(self, beta=1.0):
+        return float(self.fill("exp", {"beta": beta}, 1)[0].item())
+
+    @_op
+    def gamma(self, alpha, theta=1.0):
+        return float(self.fill("gamma", {"alpha": alpha, "theta": theta}, 1)[0].item())
+
+    @_op
+    def bounded_uint(self, b, width=64):
+        if width != 64:
+            raise NotImplementedError("only 64-bit bounded draws are on the B200 fill path")
+        return int(self.fill("uint64", {"b": b}, 1).tolist()[0])
+
+    @_op
+    def mvn(self, mean, cov, n=1, layout="n_d"):
+        """continuous.py:312-336: X = mean + z @ L^T, z = n*d std_norm draws (row-major),
+        L = Cholesky factor (pivoted LAPACK fallback for semidefinite S)."""
+        mean = np.asarray(mean, dtype=np.float64)
+        cov = np.asarray(cov, dtype=np.float64)
+        if mean.ndim != 1 or cov.shape != (mean.size, mean.size):
+            raise ValueError("mvn needs a length-d mean and a d x d covariance")
+        if not np.allclose(cov, cov.T, rtol=1e-9, atol=1e-12):
+            raise ValueError("mvn covariance must be symmetric")
+        if layout not in ("n_d", "d_n"):
+            raise ValueError("mvn layout must be 'n_d' or 'd_n'")
+        n = int(n)
+        if n < 1:
+            raise ValueError("mvn needs n >= 1")
+        d = mean.size
+        factor = np.ascontiguousarray(semidefinite_factor(cov))
+        dev = self._device()
+        out = torch.empty((n, d) if layout == "n_d" else (d, n), dtype=torch.float64, device=dev)
+        st = self.to_stream()
+        res = _lib.RsFillResult()
+        mptr = np.ascontiguousarray(mean)
+        _lib.check(_lib.lib.rs_mvn(ctypes.byref(st), ctypes.c_void_p(factor.ctypes.data),
+                                   mptr.ctypes.data_as(_lib.DBLP), d, n, 0 if layout == "n_d" else 1,
+                                   ctypes.c_void_p(out.data_ptr()), ctypes.byref(res), _cuda_stream_ptr(dev)))
+        self.from_stream(st)
+        self._add_tallies(res)
+        return out
+
+
+def semidefinite_factor(cov):
+    """continuous.py:293-309: numpy Cholesky, else pivoted dpstrf + reconstruction check."""
+    try:
+        return np.linalg.cholesky(cov)
+    except np.linalg.LinAlgError:
+        from scipy.linalg.lapack import dpstrf
+
+        c, piv, rank, info = dpstrf(cov, lower=1)
+        if info < 0:
+            raise ValueError("covariance factorization failed")
+        low = np.tril(c)
+        low[:, rank:] = 0.0
+        m = np.zeros_like(low)
+        m[piv - 1, :] = low
+        scale = max(1.0, float(np.abs(cov).max()))
+        if not np.allclose(m @ m.T, cov, rtol=0.0, atol=1e-8 * scale):
+            raise ValueError("mvn covariance must be positive semidefinite")
+        return m
+
+
+def fill_streams(engine, seed, spawn_prefix, j0, n_streams, dist, params, n_per_stream, device=None):
+    """Per-stream mode: row s = create(engine, seed, spawn_key=prefix + (j0 + s,)).fill(dist, params, n)
+    for s < n_streams, computed by one GPU thread per stream (sfc64's parallel form)."""
+    eid = engines.normalize(engine)
+    params = dict(params or {})
+    n_streams, n_per_stream = int(n_streams), int(n_per_stream)
+    if dist == "uint64":
+        b = int(params.get("b", 0))
+        fp, ip = [0.0] * 4, ([0, 1] if b == 1 << 64 else [b, 0])
+    else:
+        probe = Rng(engines.make(eid))
+        fp = probe._continuous_params(dist, params, 1) + [0.0] * 2
+        ip = [0, 0]
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    out = torch.empty((n_streams, n_per_stream), dtype=_out_dtype(dist), device=dev)
+    seedw = [int(w) & MASK64 for w in seed]
+    pre = [int(w) & MASK64 for w in spawn_prefix]
+    _lib.check(_lib.lib.rs_fill_streams(engines.NATIVE_ID[eid], _lib.u64_array(seedw), len(seedw),
+                                        _lib.u64_array(pre), len(pre), int(j0), n_streams, _lib.DIST_IDS[dist],
+                                        (ctypes.c_double * 4)(*fp[:4]), _lib.u64_array(ip, 4), n_per_stream,
+                                        ctypes.c_void_p(out.data_ptr()), _cuda_stream_ptr(dev)))
+    return out
