@@ -66,16 +66,73 @@ struct EngPcg {  // pcg.py:25-39 (DXSM of the pre-step state; 64-bit "cheap" mul
     }
 };
 
+// 64x64 -> 128 product with four 32x32->64 multiply-adds (IMAD.WIDE.U32). Both
+// carries are folded into the last addend: a1*b1 + hi(p1) + hi(p2) < 2^64, so the
+// only extra work is one 64-bit add on the ALU pipe (the IMAD pipe is the bound).
+RS_DEV void mul64x64(u64 a, u64 b, u64 &lo, u64 &hi) {
+    u32 a0 = (u32)a, a1 = (u32)(a >> 32), b0 = (u32)b, b1 = (u32)(b >> 32);
+    u64 p0, p1, p2, p3;
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(p0) : "r"(a0), "r"(b0));
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p1) : "r"(a1), "r"(b0), "l"(p0 >> 32));
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p2) : "r"(a0), "r"(b1), "l"((u64)(u32)p1));
+    u64 t = (p1 >> 32) + (p2 >> 32);
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p3) : "r"(a1), "r"(b1), "l"(t));
+    lo = (p2 << 32) | (u64)(u32)p0;
+    hi = p3;
+}
+
+// the same product as a 32-bit multiply-add carry chain (IMAD / IMAD.HI with .X)
+RS_DEV void mul64x64_cc(u64 a, u64 b, u64 &lo, u64 &hi) {
+    u32 a0 = (u32)a, a1 = (u32)(a >> 32), b0 = (u32)b, b1 = (u32)(b >> 32);
+    u32 r0, r1, r2, r3;
+    asm("{\n\t"
+        "mul.lo.u32 %0, %4, %6;\n\t"
+        "mul.hi.u32 %1, %4, %6;\n\t"
+        "mad.lo.cc.u32 %1, %5, %6, %1;\n\t"
+        "madc.hi.u32 %2, %5, %6, 0;\n\t"
+        "mad.lo.cc.u32 %1, %4, %7, %1;\n\t"
+        "madc.hi.cc.u32 %2, %4, %7, %2;\n\t"
+        "madc.hi.u32 %3, %5, %7, 0;\n\t"
+        "mad.lo.cc.u32 %2, %5, %7, %2;\n\t"
+        "addc.u32 %3, %3, 0;\n\t"
+        "}"
+        : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+        : "r"(a0), "r"(a1), "r"(b0), "r"(b1));
+    lo = ((u64)r1 << 32) | r0;
+    hi = ((u64)r3 << 32) | r2;
+}
+
 RS_DEV void philox4x64_10(u64 c0, u64 c1, u64 c2, u64 c3, u64 k0, u64 k1, u64 &o0, u64 &o1, u64 &o2, u64 &o3) {
     // counter.py:83-96
 #pragma unroll
     for (int r = 0; r < 10; r++) {
-        u64 hi0 = __umul64hi(0xD2E7470EE14C6C93ULL, c0), lo0 = 0xD2E7470EE14C6C93ULL * c0;
-        u64 hi1 = __umul64hi(0xCA5A826395121157ULL, c2), lo1 = 0xCA5A826395121157ULL * c2;
+        u64 lo0, hi0, lo1, hi1;
+        mul64x64(0xD2E7470EE14C6C93ULL, c0, lo0, hi0);
+        mul64x64(0xCA5A826395121157ULL, c2, lo1, hi1);
         u64 n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
         c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
         k0 += 0x9E3779B97F4A7C15ULL;
         k1 += 0xBB67AE8584CAA73BULL;
+    }
+    o0 = c0; o1 = c1; o2 = c2; o3 = c3;
+}
+
+// same bijection with the 10 round keys precomputed (read from the constant bank)
+template <int V = 0>
+RS_DEV void philox4x64_10_rk(u64 c0, u64 c1, u64 c2, u64 c3, const u64 *rk0, const u64 *rk1, u64 &o0, u64 &o1,
+                             u64 &o2, u64 &o3) {
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+        u64 lo0, hi0, lo1, hi1;
+        if constexpr (V == 0) {
+            mul64x64(0xD2E7470EE14C6C93ULL, c0, lo0, hi0);
+            mul64x64(0xCA5A826395121157ULL, c2, lo1, hi1);
+        } else {
+            mul64x64_cc(0xD2E7470EE14C6C93ULL, c0, lo0, hi0);
+            mul64x64_cc(0xCA5A826395121157ULL, c2, lo1, hi1);
+        }
+        u64 n0 = hi1 ^ c1 ^ rk0[r], n2 = hi0 ^ c3 ^ rk1[r];
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
     }
     o0 = c0; o1 = c1; o2 = c2; o3 = c3;
 }
@@ -393,14 +450,15 @@ struct NormP {
     RS_DEV void init(const ZigFast *f, const RsZigSlow *s, bool full_mantissa) {
         fast = f; slow = s; fm = full_mantissa; st = 0; att = 0; pdf = 0;
     }
-    // returns true when a sample is emitted into z
-    RS_DEV bool feed(u64 w, double &z) {
+    RS_DEV ZigFast prefetch(u64 w) const { return fast[w & 0xFF]; }
+    RS_DEV bool feed(u64 w, double &z) { return feed(w, prefetch(w), z); }
+    // returns true when a sample is emitted into z; f = fast[w & 0xFF] (prefetched)
+    RS_DEV bool feed(u64 w, ZigFast f, double &z) {
         if (st == 0) {
             att++;
             idx = (int)(w & 0xFF);
             sign = (u32)((w >> 8) & 1);
             rabs = (w >> 9) & ((1ULL << 52) - 1);
-            ZigFast f = fast[idx];
             x = (double)rabs * f.w;
             if (rabs < f.k) { z = sign ? -x : x; return true; }
             st = idx == 0 ? 2 : 1;
@@ -451,12 +509,13 @@ struct ExpP {
     RS_DEV void init(const ZigFast *f, const RsZigSlow *s, bool full_mantissa) {
         fast = f; slow = s; fm = full_mantissa; st = 0; att = 0; pdf = 0;
     }
-    RS_DEV bool feed(u64 w, double &z) {
+    RS_DEV ZigFast prefetch(u64 w) const { return fast[w & 0xFF]; }
+    RS_DEV bool feed(u64 w, double &z) { return feed(w, prefetch(w), z); }
+    RS_DEV bool feed(u64 w, ZigFast f, double &z) {
         if (st == 0) {
             att++;
             idx = (int)(w & 0xFF);
             rabs = (w >> 8) & ((1ULL << 53) - 1);
-            ZigFast f = fast[idx];
             x = (double)rabs * f.w;
             if (rabs < f.k) { z = x; return true; }
             st = idx == 0 ? 2 : 1;
@@ -500,11 +559,13 @@ struct GammaP {
         np.init(f, s, fm);
         g = p; st = 0; fresh = true; gatt = 0;
     }
-    RS_DEV bool feed(u64 w, double &out) {
+    RS_DEV ZigFast prefetch(u64 w) const { return np.prefetch(w); }
+    RS_DEV bool feed(u64 w, double &out) { return feed(w, prefetch(w), out); }
+    RS_DEV bool feed(u64 w, ZigFast f, double &out) {
         if (st == 0) {
             if (fresh) { gatt++; fresh = false; }
             double zz0;
-            if (np.feed(w, zz0)) {
+            if (np.feed(w, f, zz0)) {
                 double t = 1.0 + g.cc * zz0;
                 if (t > 0.0) { z = zz0; v = t * t * t; st = 1; }
             }
@@ -538,42 +599,54 @@ struct GammaP {
 
 struct DistStdNorm {
     typedef double out_t;
+    typedef ZigFast pre_t;
     NormP p;
+    RS_DEV pre_t prefetch(u64 w) const { return p.prefetch(w); }
     RS_DEV bool feed(u64 w, double &o) { return p.feed(w, o); }
-    RS_DEV void tally(u64 *t) { t[0] += p.att; t[1] += p.pdf; p.att = 0; p.pdf = 0; }
+    template <class TT> RS_DEV void tally(TT *t) { t[0] += p.att; t[1] += p.pdf; p.att = 0; p.pdf = 0; }
     RS_DEV void drop() { p.att = 0; p.pdf = 0; }
 };
 struct DistNorm {  // norm epilogue: float(mu) + sqrt(var) * z (continuous.py:157-158)
     typedef double out_t;
+    typedef ZigFast pre_t;
     NormP p;
     double mu, sd;
-    RS_DEV bool feed(u64 w, double &o) {
+    RS_DEV pre_t prefetch(u64 w) const { return p.prefetch(w); }
+    RS_DEV bool feed(u64 w, pre_t f, double &o) {
         double z;
-        if (!p.feed(w, z)) return false;
+        if (!p.feed(w, f, z)) return false;
         o = mu + sd * z;
         return true;
     }
-    RS_DEV void tally(u64 *t) { t[0] += p.att; t[1] += p.pdf; p.att = 0; p.pdf = 0; }
+    RS_DEV bool feed_raw(u64 w, pre_t f, double &o) { return p.feed(w, f, o); }
+    RS_DEV bool feed(u64 w, double &o) { return feed(w, prefetch(w), o); }
+    template <class TT> RS_DEV void tally(TT *t) { t[0] += p.att; t[1] += p.pdf; p.att = 0; p.pdf = 0; }
     RS_DEV void drop() { p.att = 0; p.pdf = 0; }
 };
 struct DistExp {  // beta * std_exp (continuous.py:165-169)
     typedef double out_t;
+    typedef ZigFast pre_t;
     ExpP p;
     double beta;
-    RS_DEV bool feed(u64 w, double &o) {
+    RS_DEV pre_t prefetch(u64 w) const { return p.prefetch(w); }
+    RS_DEV bool feed(u64 w, pre_t f, double &o) {
         double x;
-        if (!p.feed(w, x)) return false;
+        if (!p.feed(w, f, x)) return false;
         o = beta * x;
         return true;
     }
-    RS_DEV void tally(u64 *t) { t[2] += p.att; t[3] += p.pdf; p.att = 0; p.pdf = 0; }
+    RS_DEV bool feed(u64 w, double &o) { return feed(w, prefetch(w), o); }
+    template <class TT> RS_DEV void tally(TT *t) { t[2] += p.att; t[3] += p.pdf; p.att = 0; p.pdf = 0; }
     RS_DEV void drop() { p.att = 0; p.pdf = 0; }
 };
 struct DistGamma {
     typedef double out_t;
+    typedef ZigFast pre_t;
     GammaP p;
+    RS_DEV pre_t prefetch(u64 w) const { return p.prefetch(w); }
+    RS_DEV bool feed(u64 w, pre_t f, double &o) { return p.feed(w, f, o); }
     RS_DEV bool feed(u64 w, double &o) { return p.feed(w, o); }
-    RS_DEV void tally(u64 *t) {
+    template <class TT> RS_DEV void tally(TT *t) {
         t[0] += p.np.att; t[1] += p.np.pdf; t[4] += p.gatt;
         p.np.att = 0; p.np.pdf = 0; p.gatt = 0;
     }
@@ -585,9 +658,12 @@ struct DistBeta {  // x = gamma(a,1) then y = gamma(b,1); x/(x+y) (continuous.py
     GammaPrm ga, gb;
     int phase;
     double xa;
-    RS_DEV bool feed(u64 w, double &o) {
+    typedef ZigFast pre_t;
+    RS_DEV pre_t prefetch(u64 w) const { return p.prefetch(w); }
+    RS_DEV bool feed(u64 w, double &o) { return feed(w, prefetch(w), o); }
+    RS_DEV bool feed(u64 w, pre_t f, double &o) {
         double r;
-        if (!p.feed(w, r)) return false;
+        if (!p.feed(w, f, r)) return false;
         if (phase == 0) {
             xa = r; phase = 1; p.g = gb;
             return false;
@@ -596,7 +672,7 @@ struct DistBeta {  // x = gamma(a,1) then y = gamma(b,1); x/(x+y) (continuous.py
         phase = 0; p.g = ga;
         return true;
     }
-    RS_DEV void tally(u64 *t) {
+    template <class TT> RS_DEV void tally(TT *t) {
         t[0] += p.np.att; t[1] += p.np.pdf; t[4] += p.gatt;
         p.np.att = 0; p.np.pdf = 0; p.gatt = 0;
     }
@@ -604,34 +680,38 @@ struct DistBeta {  // x = gamma(a,1) then y = gamma(b,1); x/(x+y) (continuous.py
 };
 struct DistLemire {  // bounded_uint(rng, b, 64), discrete.py:20-39: accept iff low >= (2^64-b) % b
     typedef u64 out_t;
+    typedef int pre_t;
     u64 b, thr;
+    RS_DEV pre_t prefetch(u64) const { return 0; }
+    RS_DEV bool feed(u64 w, pre_t, u64 &o) { return feed(w, o); }
     RS_DEV bool feed(u64 w, u64 &o) {
         u64 low = w * b;
         if (low < thr) return false;
         o = __umul64hi(w, b);
         return true;
     }
-    RS_DEV void tally(u64 *) {}
+    template <class TT> RS_DEV void tally(TT *) {}
     RS_DEV void drop() {}
 };
 struct DistRaw {
     typedef u64 out_t;
     RS_DEV bool feed(u64 w, u64 &o) { o = w; return true; }
-    RS_DEV void tally(u64 *) {}
+    template <class TT> RS_DEV void tally(TT *) {}
     RS_DEV void drop() {}
 };
 struct DistU01 {
     typedef double out_t;
     bool fm;
     RS_DEV bool feed(u64 w, double &o) { o = u01_of(w, fm); return true; }
-    RS_DEV void tally(u64 *) {}
+    template <class TT> RS_DEV void tally(TT *) {}
     RS_DEV void drop() {}
 };
 
-// ----------------------------------------------------------------------------- 256-bit writer
+// ----------------------------------------------------------------------------- run writers
 // Writes a contiguous run of 8-byte elements starting at element `start` of
-// `out`; full 32-byte-aligned groups go out as one STG.256, the ragged head and
-// tail as scalar stores.
+// `out`. VecWriter8 emits full 32-byte-aligned groups as one STG.256 (used where
+// registers are cheap); VecWriter2 emits 16-byte pairs (STG.128) with two slots,
+// for the register-bound parse kernels. Ragged heads/tails are scalar stores.
 template <class T>
 struct VecWriter8 {
     T *abase;      // 32-byte aligned base
@@ -675,5 +755,29 @@ struct VecWriter8 {
         if (first == 0 && slot > 0) p[0] = v0;
         if (first <= 1 && slot > 1) p[1] = v1;
         if (first <= 2 && slot > 2) p[2] = v2;
+    }
+};
+
+template <class T>
+struct VecWriter2 {
+    T *ptr;     // next element
+    bool head;  // first element is not 16-byte aligned: it goes out alone
+    bool have;  // v0 holds the first half of a pair
+    T v0;
+    RS_DEV void init(T *out, u64 start) {
+        ptr = out + start;
+        head = ((uintptr_t)ptr & 15) != 0;
+        have = false;
+    }
+    RS_DEV void put(T v) {
+        if (head) { *ptr++ = v; head = false; return; }
+        if (!have) { v0 = v; have = true; return; }
+        u64 a = *(u64 *)&v0, b = *(u64 *)&v;
+        asm volatile("st.global.v2.b64 [%0], {%1, %2};" ::"l"(ptr), "l"(a), "l"(b) : "memory");
+        ptr += 2;
+        have = false;
+    }
+    RS_DEV void finish() {
+        if (have) *ptr = v0;
     }
 };

@@ -59,6 +59,8 @@ struct FillPlan {
     u64 prefix[CAP];
     u64 pcg_m[MAXLEV][2], pcg_a[MAXLEV][2];
     u64 rlx[MAXLEV][9];
+    u64 rk0[10], rk1[10];         // philox round keys (counter.py:95-96)
+    int vec_ok;                   // counter-based fill: outputs 32-byte aligned per block
     double fp[4];
     u64 ip[4];
     GammaPrm ga, gb;
@@ -180,11 +182,16 @@ __device__ __forceinline__ void make_dist(const FillPlan &p, const ZigFast *fast
 template <int D>
 __device__ __forceinline__ bool dist_feed(const FillPlan &p, typename DistOf<D>::type &d, u64 w,
                                           typename DistOf<D>::type::out_t &o) {
+    return dist_feed<D>(p, d, w, d.prefetch(w), o);
+}
+template <int D>
+__device__ __forceinline__ bool dist_feed(const FillPlan &p, typename DistOf<D>::type &d, u64 w,
+                                          typename DistOf<D>::type::pre_t f, typename DistOf<D>::type::out_t &o) {
     if constexpr (D == RS_DIST_NORM) {
-        if (p.raw_norm) return d.p.feed(w, o);
-        return d.feed(w, o);
+        if (p.raw_norm) return d.feed_raw(w, f, o);
+        return d.feed(w, f, o);
     } else {
-        return d.feed(w, o);
+        return d.feed(w, f, o);
     }
 }
 
@@ -196,20 +203,25 @@ __device__ __forceinline__ void stage_tables(const FillPlan &p, ZigFast *sm) {
 }
 
 // ----------------------------------------------------------------------------- x256 jump setup
-// block b: S_b = prod_{bits j of b} M[8+j] * base  (warp 0, lanes own 8 columns each)
-// then S_{b,i} = M[j] S_{b,i-2^j} doubling over the 8 in-block bits.
+// Thread t starts at engine word t*L: state = T^(t*L) * base over GF(2) (jumps.py:116-126
+// restated as 256x256 bit matrices, column-major, 8 KB each). Warp w first jumps by
+// 32*L*w using ML[1 + k] = T^(32*L*2^k) for the set bits k of w; its 32 lane states
+// then follow by chained products with ML[0] = T^L. Every product is warp-cooperative:
+// lane l owns columns 8l..8l+7 (one coalesced 256-byte read), then a 5-step xor
+// butterfly leaves the result in every lane.
 __device__ __forceinline__ void warp_matvec(const u64 *M, const u64 v[4], u64 out[4]) {
     int lane = threadIdx.x & 31;
     u64 a0 = 0, a1 = 0, a2 = 0, a3 = 0;
     u32 byte = (u32)((v[lane >> 3] >> (8 * (lane & 7))) & 0xFF);
-    const u64 *c = M + (u64)(8 * lane) * 4;
+    const ulonglong2 *c = (const ulonglong2 *)(M + (u64)(8 * lane) * 4);
 #pragma unroll
     for (int k = 0; k < 8; k++) {
         u64 m = (byte >> k) & 1 ? ~0ULL : 0ULL;
-        a0 ^= __ldg(c + 4 * k + 0) & m;
-        a1 ^= __ldg(c + 4 * k + 1) & m;
-        a2 ^= __ldg(c + 4 * k + 2) & m;
-        a3 ^= __ldg(c + 4 * k + 3) & m;
+        ulonglong2 x = __ldg(c + 2 * k), y = __ldg(c + 2 * k + 1);
+        a0 ^= x.x & m;
+        a1 ^= x.y & m;
+        a2 ^= y.x & m;
+        a3 ^= y.y & m;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -221,87 +233,70 @@ __device__ __forceinline__ void warp_matvec(const u64 *M, const u64 v[4], u64 ou
     out[0] = a0; out[1] = a1; out[2] = a2; out[3] = a3;
 }
 
-__device__ __forceinline__ void thread_matvec(const u64 *M, const u64 v[4], u64 out[4]) {
-    u64 a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-#pragma unroll 1
-    for (int w = 0; w < 4; w++) {
-        u64 x = v[w];
-        const u64 *c = M + (u64)(64 * w) * 4;
-#pragma unroll 8
-        for (int b = 0; b < 64; b++) {
-            u64 m = ((x >> b) & 1) ? ~0ULL : 0ULL;
-            ulonglong2 p = __ldg((const ulonglong2 *)(c + 4 * b));
-            ulonglong2 q = __ldg((const ulonglong2 *)(c + 4 * b + 2));
-            a0 ^= p.x & m; a1 ^= p.y & m; a2 ^= q.x & m; a3 ^= q.y & m;
-        }
-    }
-    out[0] = a0; out[1] = a1; out[2] = a2; out[3] = a3;
-}
-
 __global__ void __launch_bounds__(BLOCK) k_x256_setup(const __grid_constant__ FillPlan p, const u64 *ML,
                                                       u64 *states) {
-    __shared__ u64 st[BLOCK][4];
-    if (threadIdx.x < 32) {
-        u64 v[4] = {p.base[0], p.base[1], p.base[2], p.base[3]};
-        u32 b = blockIdx.x;
-        for (int j = 0; b; j++, b >>= 1)
-            if (b & 1) {
-                u64 o[4];
-                warp_matvec(ML + (u64)(8 + j) * 1024, v, o);
-                v[0] = o[0]; v[1] = o[1]; v[2] = o[2]; v[3] = o[3];
-            }
-        if (threadIdx.x == 0) { st[0][0] = v[0]; st[0][1] = v[1]; st[0][2] = v[2]; st[0][3] = v[3]; }
+    const u32 lane = threadIdx.x & 31;
+    const u64 w = ((u64)blockIdx.x * BLOCK + threadIdx.x) >> 5;
+    u64 v[4] = {p.base[0], p.base[1], p.base[2], p.base[3]};
+    u64 ww = w;
+    for (int k = 0; ww; k++, ww >>= 1)
+        if (ww & 1) warp_matvec(ML + (u64)(1 + k) * 1024, v, v);
+    u64 mine[4] = {v[0], v[1], v[2], v[3]};
+    for (u32 j = 1; j < 32; j++) {
+        warp_matvec(ML, v, v);
+        if (lane == j) { mine[0] = v[0]; mine[1] = v[1]; mine[2] = v[2]; mine[3] = v[3]; }
     }
-    __syncthreads();
-    for (int j = 0; j < 8; j++) {
-        int h = 1 << j;
-        if ((int)threadIdx.x < h) {
-            u64 v[4] = {st[threadIdx.x][0], st[threadIdx.x][1], st[threadIdx.x][2], st[threadIdx.x][3]};
-            u64 o[4];
-            thread_matvec(ML + (u64)j * 1024, v, o);
-            st[threadIdx.x + h][0] = o[0]; st[threadIdx.x + h][1] = o[1];
-            st[threadIdx.x + h][2] = o[2]; st[threadIdx.x + h][3] = o[3];
-        }
-        __syncthreads();
-    }
-    u64 t = (u64)blockIdx.x * BLOCK + threadIdx.x;
-    ulonglong2 *d = (ulonglong2 *)(states + 4 * t);
-    d[0] = make_ulonglong2(st[threadIdx.x][0], st[threadIdx.x][1]);
-    d[1] = make_ulonglong2(st[threadIdx.x][2], st[threadIdx.x][3]);
+    ulonglong2 *d = (ulonglong2 *)(states + 4 * (32 * w + lane));
+    d[0] = make_ulonglong2(mine[0], mine[1]);
+    d[1] = make_ulonglong2(mine[2], mine[3]);
+}
+
+// resident blocks per SM the parse kernels are compiled for (register budget)
+constexpr int minb(int E, int D) {
+    return E == RS_ENG_RANLUX ? 2 : (D == RS_DIST_GAMMA || D == RS_DIST_BETA) ? 2 : D == RS_DIST_UINT64 ? 4 : 3;
 }
 
 // ----------------------------------------------------------------------------- parse loop
 // Parses from logical position `pos` (a boundary) until the first boundary at or
 // beyond `end`, or until `maxc` samples were emitted. Returns samples emitted.
-template <int E, int D, bool EMIT, class W>
+template <int E, int D, bool EMIT, class W, class TT>
 __device__ __forceinline__ u64 parse(const FillPlan &p, Src<E> &s, typename DistOf<D>::type &d, u64 &pos, u64 end,
-                                     u64 maxc, W *wr, u64 *tally, u64 &last_end) {
+                                     u64 maxc, W *wr, TT *tally, u64 &last_end) {
     typedef typename DistOf<D>::type::out_t T;
     u64 c = 0;
     if (maxc == 0) return 0;
     bool boundary = true;
+    // words are generated four at a time so the engine's dependency chain overlaps the
+    // parse; words generated past the exit are simply dropped (only `pos` matters)
     while (true) {
-        if (boundary && pos >= end) break;
-        u64 w = s.next();
-        pos++;
-        T v;
-        if (dist_feed<D>(p, d, w, v)) {
-            boundary = true;
-            if constexpr (EMIT) {
-                wr->put(v);
-                d.tally(tally);
-                last_end = pos;
+        u64 w[4];
+        typename DistOf<D>::type::pre_t f[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) w[k] = s.next();
+#pragma unroll
+        for (int k = 0; k < 4; k++) f[k] = d.prefetch(w[k]);  // table loads issued together
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            if (boundary && pos >= end) return c;
+            pos++;
+            T v;
+            if (dist_feed<D>(p, d, w[k], f[k], v)) {
+                boundary = true;
+                if constexpr (EMIT) {
+                    wr->put(v);
+                    d.tally(tally);
+                    last_end = pos;
+                }
+                if (++c >= maxc) return c;
+            } else {
+                boundary = false;
             }
-            if (++c >= maxc) break;
-        } else {
-            boundary = false;
         }
     }
-    return c;
 }
 
 template <int E, int D>
-__global__ void __launch_bounds__(BLOCK) k_count(const __grid_constant__ FillPlan p, u64 *cnt0, u32 *ex0) {
+__global__ void __launch_bounds__(BLOCK, minb(E, D)) k_count(const __grid_constant__ FillPlan p, u64 *cnt0, u32 *ex0) {
     __shared__ ZigFast sm[256];
     stage_tables(p, sm);
     u32 t = blockIdx.x * BLOCK + threadIdx.x;
@@ -312,7 +307,7 @@ __global__ void __launch_bounds__(BLOCK) k_count(const __grid_constant__ FillPla
     typename DistOf<D>::type d;
     make_dist<D>(p, sm, d);
     u64 dummy;
-    u64 c = parse<E, D, false, VecWriter8<u64>>(p, s, d, pos, end, ~0ULL, nullptr, nullptr, dummy);
+    u64 c = parse<E, D, false, VecWriter8<u64>, u32>(p, s, d, pos, end, ~0ULL, nullptr, nullptr, dummy);
     cnt0[t] = c;
     ex0[t] = (u32)(pos - end);
 }
@@ -362,7 +357,7 @@ __device__ void resolve_entry(const FillPlan &p, const ZigFast *sm, u32 t, u32 e
 
 // round 0: prev_ex = ex0, every thread; round r>0: only threads whose entry changed.
 template <int E, int D>
-__global__ void __launch_bounds__(BLOCK) k_fixup(const __grid_constant__ FillPlan p, const u64 *cnt0, const u32 *ex0,
+__global__ void __launch_bounds__(BLOCK, minb(E, D)) k_fixup(const __grid_constant__ FillPlan p, const u64 *cnt0, const u32 *ex0,
                                                  const u32 *prev_ex, u32 *entry, u64 *cnt, u32 *ex, int round,
                                                  DevResult *res) {
     __shared__ ZigFast sm[256];
@@ -389,12 +384,12 @@ __global__ void __launch_bounds__(BLOCK) k_fixup(const __grid_constant__ FillPla
 }
 
 template <int E, int D>
-__global__ void __launch_bounds__(BLOCK) k_emit(const __grid_constant__ FillPlan p, const u32 *entry, const u64 *cnt,
+__global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constant__ FillPlan p, const u32 *entry, const u64 *cnt,
                                                 const u64 *off, const u32 *ex, DevResult *res) {
     __shared__ ZigFast sm[256];
     stage_tables(p, sm);
     u32 t = blockIdx.x * BLOCK + threadIdx.x;
-    u64 tally[6] = {0, 0, 0, 0, 0, 0};
+    u32 tally[6] = {0, 0, 0, 0, 0, 0};
     if (t < p.T) {
         u64 o = off[t], c = cnt[t];
         if (t == p.T - 1) {
@@ -409,7 +404,7 @@ __global__ void __launch_bounds__(BLOCK) k_emit(const __grid_constant__ FillPlan
             typename DistOf<D>::type d;
             make_dist<D>(p, sm, d);
             typedef typename DistOf<D>::type::out_t T;
-            VecWriter8<T> wr;
+            VecWriter2<T> wr;
             wr.init((T *)p.out, p.out0 + o);
             u64 last_end = 0;
             parse<E, D, true>(p, s, d, pos, ~0ULL, kmax, &wr, tally, last_end);
@@ -421,7 +416,7 @@ __global__ void __launch_bounds__(BLOCK) k_emit(const __grid_constant__ FillPlan
 #pragma unroll
     for (int i = 0; i < 6; i++) {
         u64 v = tally[i];
-        for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, s);
+        for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, s);  // u64: no overflow
         if ((threadIdx.x & 31) == 0 && v) atomicAdd((unsigned long long *)&res->tally[i], (unsigned long long)v);
     }
 }
@@ -485,6 +480,63 @@ __global__ void __launch_bounds__(BLOCK) k_fixed(const __grid_constant__ FillPla
             u64 w = 0;
             for (u64 i = lim; i <= full_words; i++) w = s.next();
             o2[2 * full_words] = u01f_of((u32)w, p.fm);
+        }
+    }
+}
+
+// Counter-based fixed fills (Philox-4x64-10, counter.py:98-121): word w of the
+// stream is block(ctr0 + w/4)[w % 4], so threads take lane-consecutive blocks in
+// a grid-stride loop and each warp store is one contiguous 1 KB (STG.256 per lane).
+template <int MODE, int V = 0>
+__global__ void __launch_bounds__(BLOCK) k_philox_fixed(const __grid_constant__ FillPlan p) {
+    const u64 nblk = (p.weng + 3) / 4;
+    const u64 stride = (u64)gridDim.x * BLOCK;
+    u64 b = (u64)blockIdx.x * BLOCK + threadIdx.x;
+    if (b == 0) {  // the buffered prefix and a pending half (thread 0)
+        if constexpr (MODE == FX_U01F) {
+            float *out = (float *)p.out;
+            if (p.pending_used) out[0] = u01f_of(p.pending_val, p.fm);
+            for (int i = 0; i < p.P; i++) {
+                u64 f = (u64)p.pending_used + 2ULL * i;
+                if (f < p.n) out[f] = u01f_of((u32)p.prefix[i], p.fm);
+                if (f + 1 < p.n) out[f + 1] = u01f_of((u32)(p.prefix[i] >> 32), p.fm);
+            }
+        } else {
+            u64 *out = (u64 *)p.out;
+            for (int i = 0; i < p.P && (u64)i < p.n; i++) out[i] = fx_map<MODE>(p, p.prefix[i]);
+        }
+    }
+    for (; b < nblk; b += stride) {
+        u64 c0 = p.base[0] + b, c1 = p.base[1], c2 = p.base[2], c3 = p.base[3];
+        if (c0 < b) { if (++c1 == 0) { if (++c2 == 0) ++c3; } }
+        u64 w0, w1, w2, w3;
+        philox4x64_10_rk<V>(c0, c1, c2, c3, p.rk0, p.rk1, w0, w1, w2, w3);
+        if constexpr (MODE == FX_U01F) {
+            u64 f = (u64)p.pending_used + 2ULL * ((u64)p.P + 4 * b);  // first f32 index of this block
+            u64 q0 = fx_map<MODE>(p, w0), q1 = fx_map<MODE>(p, w1), q2 = fx_map<MODE>(p, w2), q3 = fx_map<MODE>(p, w3);
+            float *out = (float *)p.out;
+            if (p.vec_ok && f + 8 <= p.n) {
+                asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(out + f), "l"(q0), "l"(q1), "l"(q2),
+                             "l"(q3) : "memory");
+            } else {
+                u64 q[4] = {q0, q1, q2, q3};
+#pragma unroll
+                for (int i = 0; i < 8; i++)
+                    if (f + i < p.n) out[f + i] = __uint_as_float((u32)(q[i >> 1] >> (32 * (i & 1))));
+            }
+        } else {
+            u64 e = (u64)p.P + 4 * b;
+            u64 q0 = fx_map<MODE>(p, w0), q1 = fx_map<MODE>(p, w1), q2 = fx_map<MODE>(p, w2), q3 = fx_map<MODE>(p, w3);
+            u64 *out = (u64 *)p.out;
+            if (p.vec_ok && e + 4 <= p.n) {
+                asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(out + e), "l"(q0), "l"(q1), "l"(q2),
+                             "l"(q3) : "memory");
+            } else {
+                if (e < p.n) out[e] = q0;
+                if (e + 1 < p.n) out[e + 1] = q1;
+                if (e + 2 < p.n) out[e + 2] = q2;
+                if (e + 3 < p.n) out[e + 3] = q3;
+            }
         }
     }
 }
@@ -742,23 +794,28 @@ rs_status ensure_scratch(DevCtx &c, size_t T) {
     return RS_OK;
 }
 
-// x256: M_j = T^(L * 2^j), j < levels; cached per (L, levels) on the device
+// x256: ML[0] = T^L, ML[1 + k] = T^(32 L 2^k) for k < levels; cached per (L, levels) on the device
 rs_status x256_mats(DevCtx &c, u64 L, int levels, u64 **out) {
     auto key = std::make_pair(L, levels);
     auto it = c.x256_ml.find(key);
     if (it != c.x256_ml.end()) { *out = it->second; return RS_OK; }
-    std::vector<rs::Mat256> m(levels);
-    // T^L from the T^(2^k) table
+    std::vector<rs::Mat256> m(1 + levels);
     bool init = false;
     for (int k = 0; k < 64; k++)
         if ((L >> k) & 1) {
             if (!init) { m[0] = rs::x256_pow2(k); init = true; }
             else rs::mat_mul(rs::x256_pow2(k), m[0], m[0]);
         }
-    for (int j = 1; j < levels; j++) rs::mat_mul(m[j - 1], m[j - 1], m[j]);
+    if (levels > 0) {
+        rs::Mat256 *t = new rs::Mat256(m[0]);
+        for (int i = 0; i < 5; i++) rs::mat_mul(*t, *t, *t);  // T^(32 L)
+        m[1] = *t;
+        delete t;
+        for (int k = 1; k < levels; k++) rs::mat_mul(m[k], m[k], m[k + 1]);
+    }
     u64 *d;
-    CK(cudaMalloc(&d, (size_t)levels * sizeof(rs::Mat256)));
-    CK(cudaMemcpy(d, m.data(), (size_t)levels * sizeof(rs::Mat256), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&d, (size_t)(1 + levels) * sizeof(rs::Mat256)));
+    CK(cudaMemcpy(d, m.data(), (size_t)(1 + levels) * sizeof(rs::Mat256), cudaMemcpyHostToDevice));
     if (c.x256_ml.size() > 16) {  // bound the cache
         for (auto &kv : c.x256_ml) cudaFree(kv.second);
         c.x256_ml.clear();
@@ -766,6 +823,19 @@ rs_status x256_mats(DevCtx &c, u64 L, int levels, u64 **out) {
     c.x256_ml[key] = d;
     *out = d;
     return RS_OK;
+}
+
+int occupancy(const void *fn) {
+    static std::map<const void *, int> cache;
+    auto it = cache.find(fn);
+    if (it != cache.end()) return it->second;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BLOCK, 0) != cudaSuccess || nb < 1) {
+        cudaGetLastError();
+        nb = 1;
+    }
+    cache[fn] = nb;
+    return nb;
 }
 
 bool is_device_ptr(const void *p) {
@@ -828,6 +898,23 @@ const void *fixed_kernel(int e, int mode) {
     case RS_ENG_PCG64: return fixed_kernel_e<RS_ENG_PCG64>(mode);
     case RS_ENG_PHILOX: return fixed_kernel_e<RS_ENG_PHILOX>(mode);
     default: return fixed_kernel_e<RS_ENG_RANLUX>(mode);
+    }
+}
+const void *philox_kernel(int mode) {
+    static int variant = getenv("RS_PHILOX_VARIANT") ? atoi(getenv("RS_PHILOX_VARIANT")) : 0;
+    if (variant == 1) {
+        switch (mode) {
+        case FX_RAW: return (const void *)k_philox_fixed<FX_RAW, 1>;
+        case FX_U01: return (const void *)k_philox_fixed<FX_U01, 1>;
+        case FX_POW2: return (const void *)k_philox_fixed<FX_POW2, 1>;
+        default: return (const void *)k_philox_fixed<FX_U01F, 1>;
+        }
+    }
+    switch (mode) {
+    case FX_RAW: return (const void *)k_philox_fixed<FX_RAW>;
+    case FX_U01: return (const void *)k_philox_fixed<FX_U01>;
+    case FX_POW2: return (const void *)k_philox_fixed<FX_POW2>;
+    default: return (const void *)k_philox_fixed<FX_U01F>;
     }
 }
 const void *serial_kernel(int d, int fixed_mode) {
@@ -944,8 +1031,9 @@ void fill_plan_common(FillPlan &p, DevCtx &c, const Resolved &r, int engine, int
 }
 
 // Segment geometry + per-engine jump tables for stride L (engine origin = p.base)
-rs_status plan_segments(DevCtx &c, FillPlan &p, u64 words, u64 Lmin, cudaStream_t st) {
-    u64 Tfull = (u64)c.sms * 4 * BLOCK;
+rs_status plan_segments(DevCtx &c, FillPlan &p, u64 words, u64 Lmin, int occ, cudaStream_t st) {
+    // exactly one wave of resident threads: equal segments finish together
+    u64 Tfull = (u64)c.sms * (u64)occ * BLOCK;
     u64 L = (words + Tfull - 1) / Tfull;
     if (L < Lmin) L = Lmin;
     L = (L + 35) / 36 * 36;  // a whole number of philox blocks and ranlux chunks
@@ -970,7 +1058,8 @@ rs_status plan_segments(DevCtx &c, FillPlan &p, u64 words, u64 Lmin, cudaStream_
     } else if (p.engine == RS_ENG_RANLUX) {
         for (int j = 0; j < levels; j++) rs::rlx_pow_A((u128)(L / 9) << j, p.rlx[j]);
     } else if (p.engine == RS_ENG_X256SS || p.engine == RS_ENG_X256PP) {
-        int lv = levels < 8 ? 8 : levels;
+        int lv = 0;  // bits of the warp index
+        while ((1ULL << lv) < T / 32) lv++;
         u64 *ml;
         s = x256_mats(c, L, lv, &ml);
         if (s) return s;
@@ -1089,10 +1178,35 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
         p.n = n;
         p.weng = words > (u64)p.P ? words - p.P : 0;
         if (r.fixed_mode == FX_POW2) p.ip[0] = r.ip[0];
-        rc = plan_segments(c, p, p.weng ? p.weng : 1, 64, st);
+        if (s->engine == RS_ENG_PHILOX) {
+            const void *fn = philox_kernel(r.fixed_mode);
+            // round keys k + r*W (counter.py:95-96) live in the constant bank
+            for (int i = 0; i < 10; i++) {
+                p.rk0[i] = p.base[4] + (u64)i * 0x9E3779B97F4A7C15ULL;
+                p.rk1[i] = p.base[5] + (u64)i * 0xBB67AE8584CAA73BULL;
+            }
+            uintptr_t a = (uintptr_t)dout;
+            if (r.fixed_mode == FX_U01F)
+                p.vec_ok = ((a + 4 * ((u64)p.pending_used + 2ULL * p.P)) & 31) == 0;
+            else
+                p.vec_ok = ((a + 8ULL * p.P) & 31) == 0;
+            u64 nblk = (p.weng + 3) / 4;
+            u64 g = (u64)c.sms * occupancy(fn);
+            u64 need = (nblk + BLOCK - 1) / BLOCK;
+            if (need < g) g = need;
+            if (g < 1) g = 1;
+            void *args[] = {&p};
+            rc = launch(fn, dim3((unsigned)g), dim3(BLOCK), args, st);
+            if (rc) return rc;
+            E = words;
+            chunks = 1;
+            return RS_OK;
+        }
+        const void *fn = fixed_kernel(s->engine, r.fixed_mode);
+        rc = plan_segments(c, p, p.weng ? p.weng : 1, 64, occupancy(fn), st);
         if (rc) return rc;
         void *args[] = {&p};
-        rc = launch(fixed_kernel(s->engine, r.fixed_mode), dim3(p.T / BLOCK), dim3(BLOCK), args, st);
+        rc = launch(fn, dim3(p.T / BLOCK), dim3(BLOCK), args, st);
         if (rc) return rc;
         E = words;
         chunks = 1;
@@ -1125,7 +1239,8 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
         p.lp0 = lp0;
         p.n = need;
         p.out0 = done;
-        rc = plan_segments(c, p, words + lp0, Lmin, st);
+        int occ = std::min(occupancy(K.count), std::min(occupancy(K.fixup), occupancy(K.emit)));
+        rc = plan_segments(c, p, words + lp0, Lmin, occ, st);
         if (rc) return rc;
         CK(cudaMemsetAsync(c.res, 0, offsetof(DevResult, serial_state), st));
         unsigned g = p.T / BLOCK;
