@@ -417,12 +417,21 @@ __device__ __noinline__ double det_log_dev(double x) {
     return dk * ln2hi - ((s * (f - R) - dk * ln2lo) - f);
 }
 
-// ----------------------------------------------------------------------------- parsers
+// ----------------------------------------------------------------------------- samplers
+// The reference samplers restated as device functions that pull words from a
+// source `S` (anything with `u64 next()`), in exactly the reference's draw order.
+// One call = one sample, so the source position after a call is a sample
+// boundary -- the only points where the reference's call stack carries no state.
+// Tallies (attempts / density evaluations, continuous.py:32-33) accumulate into
+// the caller's counters.
 
-// The fast-path strip {K, W} (16 B) lives in shared memory; slow-path data in global.
-struct ZigFast {
+struct ZigFast {  // 16-byte fast-path strip {K, W}, staged in shared memory
     u64 k;
     double w;
+};
+
+struct Tally {
+    u32 norm_att, norm_pdf, exp_att, exp_pdf, gamma_att;
 };
 
 RS_DEV bool lt128(u64 alo, u64 ahi, u64 blo, u64 bhi) { return ahi < bhi || (ahi == bhi && alo < blo); }
@@ -435,276 +444,155 @@ RS_DEV void zig_lhs(u64 yv, u64 d, u64 rk, u64 &lo, u64 &hi) {
     hi = phi + shi + (lo < plo ? 1ULL : 0ULL);
 }
 
-// std_norm, continuous.py:40-68.  Tallies: norm attempts / pdf_evals of the
-// current (not yet emitted) sample.
-struct NormP {
-    const ZigFast *fast;  // smem, 256 strips
+struct ZigCtx {
+    const ZigFast *fast;  // shared memory
     const RsZigSlow *slow;
-    bool fm;
-    int st;  // 0 start, 1 slow (second word), 2 tail xx, 3 tail yy
-    int idx;
-    u32 sign;
-    u64 rabs;
-    double x, xx;
-    u32 att, pdf;
-    RS_DEV void init(const ZigFast *f, const RsZigSlow *s, bool full_mantissa) {
-        fast = f; slow = s; fm = full_mantissa; st = 0; att = 0; pdf = 0;
-    }
-    RS_DEV ZigFast prefetch(u64 w) const { return fast[w & 0xFF]; }
-    RS_DEV bool feed(u64 w, double &z) { return feed(w, prefetch(w), z); }
-    // returns true when a sample is emitted into z; f = fast[w & 0xFF] (prefetched)
-    RS_DEV bool feed(u64 w, ZigFast f, double &z) {
-        if (st == 0) {
-            att++;
-            idx = (int)(w & 0xFF);
-            sign = (u32)((w >> 8) & 1);
-            rabs = (w >> 9) & ((1ULL << 52) - 1);
-            x = (double)rabs * f.w;
-            if (rabs < f.k) { z = sign ? -x : x; return true; }
-            st = idx == 0 ? 2 : 1;
-            return false;
-        }
-        if (st == 1) {
-            st = 0;
-            u64 yv = w >> 12;
-            u64 K = __ldg(&slow->k[idx]);
-            u64 lo, hi;
-            zig_lhs(yv, (1ULL << 52) - K, rabs - K, lo, hi);
-            if (lt128(lo, hi, __ldg(&slow->ta_lo[idx]), __ldg(&slow->ta_hi[idx]))) { z = sign ? -x : x; return true; }
-            if (!lt128(__ldg(&slow->tr_lo[idx]), __ldg(&slow->tr_hi[idx]), lo, hi)) {
-                pdf++;
-                double fi = __ldg(&slow->f[idx]), fim1 = __ldg(&slow->f[idx - 1]);
-                double y = fi + ((double)yv * 2.220446049250313e-16) * (fim1 - fi);
-                if (y < det_exp_dev(-0.5 * x * x)) { z = sign ? -x : x; return true; }
-            }
-            return false;  // reject: a fresh attempt starts at the next word
-        }
-        if (st == 2) {
-            xx = -dbl(RS_NOR_INV_R_BITS) * det_log_dev(1.0 - u01_of(w, fm));
-            st = 3;
-            return false;
-        }
-        double yy = -det_log_dev(1.0 - u01_of(w, fm));
-        if (yy + yy > xx * xx) {
-            double t = dbl(RS_NOR_R_BITS) + xx;
-            z = sign ? -t : t;
-            st = 0;
-            return true;
-        }
-        st = 2;
-        return false;
-    }
+    bool fm;              // full-mantissa u01 inside tails / gamma (rng.py:98-106)
 };
 
-// std_exp, continuous.py:71-93
-struct ExpP {
-    const ZigFast *fast;
-    const RsZigSlow *slow;
-    bool fm;
-    int st;
-    int idx;
-    u64 rabs;
-    double x;
-    u32 att, pdf;
-    RS_DEV void init(const ZigFast *f, const RsZigSlow *s, bool full_mantissa) {
-        fast = f; slow = s; fm = full_mantissa; st = 0; att = 0; pdf = 0;
-    }
-    RS_DEV ZigFast prefetch(u64 w) const { return fast[w & 0xFF]; }
-    RS_DEV bool feed(u64 w, double &z) { return feed(w, prefetch(w), z); }
-    RS_DEV bool feed(u64 w, ZigFast f, double &z) {
-        if (st == 0) {
-            att++;
-            idx = (int)(w & 0xFF);
-            rabs = (w >> 8) & ((1ULL << 53) - 1);
-            x = (double)rabs * f.w;
-            if (rabs < f.k) { z = x; return true; }
-            st = idx == 0 ? 2 : 1;
-            return false;
-        }
-        if (st == 1) {
-            st = 0;
-            u64 yv = w >> 12;
-            u64 K = __ldg(&slow->k[idx]);
-            u64 lo, hi;
-            zig_lhs(yv, (1ULL << 53) - K, rabs - K, lo, hi);
-            if (lt128(lo, hi, __ldg(&slow->ta_lo[idx]), __ldg(&slow->ta_hi[idx]))) { z = x; return true; }
-            if (!lt128(__ldg(&slow->tr_lo[idx]), __ldg(&slow->tr_hi[idx]), lo, hi)) {
-                pdf++;
-                double fe = __ldg(&slow->f[idx]), fem1 = __ldg(&slow->f[idx - 1]);
-                double y = fe + ((double)yv * 2.220446049250313e-16) * (fem1 - fe);
-                if (y < det_exp_dev(-x)) { z = x; return true; }
+// std_norm, continuous.py:40-68
+template <class S>
+RS_DEV double std_norm(S &s, const ZigCtx &z, Tally &t) {
+    while (true) {
+        t.norm_att++;
+        u64 w = s.next();
+        int idx = (int)(w & 0xFF);
+        u64 rabs = (w >> 9) & ((1ULL << 52) - 1);
+        ZigFast f = z.fast[idx];
+        double x = (double)rabs * f.w;
+        bool neg = (w >> 8) & 1;
+        if (rabs < f.k) return neg ? -x : x;
+        if (idx == 0) {  // Marsaglia tail: pairs of uniforms until accepted
+            while (true) {
+                double xx = -dbl(RS_NOR_INV_R_BITS) * det_log_dev(1.0 - u01_of(s.next(), z.fm));
+                double yy = -det_log_dev(1.0 - u01_of(s.next(), z.fm));
+                if (yy + yy > xx * xx) {
+                    double r = dbl(RS_NOR_R_BITS) + xx;
+                    return neg ? -r : r;
+                }
             }
-            return false;
         }
-        z = dbl(RS_EXP_R_BITS) - det_log_dev(1.0 - u01_of(w, fm));
-        st = 0;
-        return true;
+        u64 yv = s.next() >> 12;
+        u64 K = __ldg(&z.slow->k[idx]);
+        u64 lo, hi;
+        zig_lhs(yv, (1ULL << 52) - K, rabs - K, lo, hi);
+        if (lt128(lo, hi, __ldg(&z.slow->ta_lo[idx]), __ldg(&z.slow->ta_hi[idx]))) return neg ? -x : x;
+        if (!lt128(__ldg(&z.slow->tr_lo[idx]), __ldg(&z.slow->tr_hi[idx]), lo, hi)) {
+            t.norm_pdf++;
+            double fi = __ldg(&z.slow->f[idx]), fim1 = __ldg(&z.slow->f[idx - 1]);
+            double y = fi + ((double)yv * 2.220446049250313e-16) * (fim1 - fi);
+            if (y < det_exp_dev(-0.5 * x * x)) return neg ? -x : x;
+        }
     }
-};
+}
+
+// std_exp, continuous.py:71-93
+template <class S>
+RS_DEV double std_exp(S &s, const ZigCtx &z, Tally &t) {
+    while (true) {
+        t.exp_att++;
+        u64 w = s.next();
+        int idx = (int)(w & 0xFF);
+        u64 rabs = (w >> 8) & ((1ULL << 53) - 1);
+        ZigFast f = z.fast[idx];
+        double x = (double)rabs * f.w;
+        if (rabs < f.k) return x;
+        if (idx == 0) return dbl(RS_EXP_R_BITS) - det_log_dev(1.0 - u01_of(s.next(), z.fm));
+        u64 yv = s.next() >> 12;
+        u64 K = __ldg(&z.slow->k[idx]);
+        u64 lo, hi;
+        zig_lhs(yv, (1ULL << 53) - K, rabs - K, lo, hi);
+        if (lt128(lo, hi, __ldg(&z.slow->ta_lo[idx]), __ldg(&z.slow->ta_hi[idx]))) return x;
+        if (!lt128(__ldg(&z.slow->tr_lo[idx]), __ldg(&z.slow->tr_hi[idx]), lo, hi)) {
+            t.exp_pdf++;
+            double fe = __ldg(&z.slow->f[idx]), fem1 = __ldg(&z.slow->f[idx - 1]);
+            double y = fe + ((double)yv * 2.220446049250313e-16) * (fem1 - fe);
+            if (y < det_exp_dev(-x)) return x;
+        }
+    }
+}
 
 // Marsaglia-Tsang gamma with the power-of-uniform boost below 1, continuous.py:183-212.
 struct GammaPrm {
-    double d, cc, td;   // d = a-1/3, cc = 1/sqrt(9d), td = theta*d (alpha >= 1 core)
+    double d, cc, td;  // d = a-1/3, cc = 1/sqrt(9d), td = theta*d (for the alpha >= 1 core)
     double alpha, theta;
-    int boost;          // alpha < 1: core runs gamma(alpha+1, 1)
+    int boost;         // alpha < 1: core runs gamma(alpha+1, 1), then the U^(1/alpha) boost
 };
-struct GammaP {
-    NormP np;
-    GammaPrm g;
-    int st;        // 0 need z (normal sub-parser), 1 need u, 2 need boost u
-    bool fresh;    // next z-word starts a new attempt
-    double z, v, base;
-    u32 gatt;
-    RS_DEV void init(const ZigFast *f, const RsZigSlow *s, bool fm, const GammaPrm &p) {
-        np.init(f, s, fm);
-        g = p; st = 0; fresh = true; gatt = 0;
+
+template <class S>
+RS_DEV double gamma_core(S &s, const ZigCtx &z, const GammaPrm &g, Tally &t) {
+    while (true) {
+        t.gamma_att++;
+        double zn, tt;
+        do {
+            zn = std_norm(s, z, t);
+            tt = 1.0 + g.cc * zn;
+        } while (!(tt > 0.0));
+        double v = tt * tt * tt;
+        double u = u01_of(s.next(), z.fm);
+        double zz = zn * zn;
+        if (u < 1.0 - 0.0331 * zz * zz) return g.td * v;
+        if (det_log_dev(u) < 0.5 * zz + g.d - g.d * v + g.d * det_log_dev(v)) return g.td * v;
     }
-    RS_DEV ZigFast prefetch(u64 w) const { return np.prefetch(w); }
-    RS_DEV bool feed(u64 w, double &out) { return feed(w, prefetch(w), out); }
-    RS_DEV bool feed(u64 w, ZigFast f, double &out) {
-        if (st == 0) {
-            if (fresh) { gatt++; fresh = false; }
-            double zz0;
-            if (np.feed(w, f, zz0)) {
-                double t = 1.0 + g.cc * zz0;
-                if (t > 0.0) { z = zz0; v = t * t * t; st = 1; }
-            }
-            return false;
-        }
-        if (st == 1) {
-            double u = u01_of(w, np.fm);
-            double zz = z * z;
-            bool acc = u < 1.0 - 0.0331 * zz * zz;
-            if (!acc) acc = det_log_dev(u) < 0.5 * zz + g.d - g.d * v + g.d * det_log_dev(v);
-            st = 0;
-            fresh = true;
-            if (!acc) return false;
-            double r = g.td * v;
-            if (!g.boost) { out = r; return true; }
-            base = r;
-            st = 2;
-            return false;
-        }
-        // boost: theta * base * det_exp(det_log(u) / alpha)
-        double u = u01_of(w, np.fm);
-        out = g.theta * base * det_exp_dev(det_log_dev(u) / g.alpha);
-        st = 0;
-        return true;
-    }
-};
+}
+
+template <class S>
+RS_DEV double gamma_sample(S &s, const ZigCtx &z, const GammaPrm &g, Tally &t) {
+    double r = gamma_core(s, z, g, t);
+    if (!g.boost) return r;
+    double u = u01_of(s.next(), z.fm);
+    return g.theta * r * det_exp_dev(det_log_dev(u) / g.alpha);
+}
 
 // ----------------------------------------------------------------------------- distributions
-// A Dist turns the word stream into samples: feed(w, out) returns true on an
-// emission; tally(t6) moves the finished sample's diagnostics into t6[6].
+// A Dist draws one sample per call to sample(s, t).
 
-struct DistStdNorm {
+struct DistNorm {  // norm: float(mu) + sqrt(var) * z (continuous.py:157-158); raw = std_norm (mvn z)
     typedef double out_t;
-    typedef ZigFast pre_t;
-    NormP p;
-    RS_DEV pre_t prefetch(u64 w) const { return p.prefetch(w); }
-    RS_DEV bool feed(u64 w, double &o) { return p.feed(w, o); }
-    template <class TT> RS_DEV void tally(TT *t) { t[0] += p.att; t[1] += p.pdf; p.att = 0; p.pdf = 0; }
-    RS_DEV void drop() { p.att = 0; p.pdf = 0; }
-};
-struct DistNorm {  // norm epilogue: float(mu) + sqrt(var) * z (continuous.py:157-158)
-    typedef double out_t;
-    typedef ZigFast pre_t;
-    NormP p;
+    ZigCtx z;
     double mu, sd;
-    RS_DEV pre_t prefetch(u64 w) const { return p.prefetch(w); }
-    RS_DEV bool feed(u64 w, pre_t f, double &o) {
-        double z;
-        if (!p.feed(w, f, z)) return false;
-        o = mu + sd * z;
-        return true;
+    int raw;
+    template <class S> RS_DEV double sample(S &s, Tally &t) const {
+        double v = std_norm(s, z, t);
+        return raw ? v : mu + sd * v;
     }
-    RS_DEV bool feed_raw(u64 w, pre_t f, double &o) { return p.feed(w, f, o); }
-    RS_DEV bool feed(u64 w, double &o) { return feed(w, prefetch(w), o); }
-    template <class TT> RS_DEV void tally(TT *t) { t[0] += p.att; t[1] += p.pdf; p.att = 0; p.pdf = 0; }
-    RS_DEV void drop() { p.att = 0; p.pdf = 0; }
 };
 struct DistExp {  // beta * std_exp (continuous.py:165-169)
     typedef double out_t;
-    typedef ZigFast pre_t;
-    ExpP p;
+    ZigCtx z;
     double beta;
-    RS_DEV pre_t prefetch(u64 w) const { return p.prefetch(w); }
-    RS_DEV bool feed(u64 w, pre_t f, double &o) {
-        double x;
-        if (!p.feed(w, f, x)) return false;
-        o = beta * x;
-        return true;
-    }
-    RS_DEV bool feed(u64 w, double &o) { return feed(w, prefetch(w), o); }
-    template <class TT> RS_DEV void tally(TT *t) { t[2] += p.att; t[3] += p.pdf; p.att = 0; p.pdf = 0; }
-    RS_DEV void drop() { p.att = 0; p.pdf = 0; }
+    template <class S> RS_DEV double sample(S &s, Tally &t) const { return beta * std_exp(s, z, t); }
 };
 struct DistGamma {
     typedef double out_t;
-    typedef ZigFast pre_t;
-    GammaP p;
-    RS_DEV pre_t prefetch(u64 w) const { return p.prefetch(w); }
-    RS_DEV bool feed(u64 w, pre_t f, double &o) { return p.feed(w, f, o); }
-    RS_DEV bool feed(u64 w, double &o) { return p.feed(w, o); }
-    template <class TT> RS_DEV void tally(TT *t) {
-        t[0] += p.np.att; t[1] += p.np.pdf; t[4] += p.gatt;
-        p.np.att = 0; p.np.pdf = 0; p.gatt = 0;
-    }
-    RS_DEV void drop() { p.np.att = 0; p.np.pdf = 0; p.gatt = 0; }
+    ZigCtx z;
+    GammaPrm g;
+    template <class S> RS_DEV double sample(S &s, Tally &t) const { return gamma_sample(s, z, g, t); }
 };
 struct DistBeta {  // x = gamma(a,1) then y = gamma(b,1); x/(x+y) (continuous.py:215-218)
     typedef double out_t;
-    GammaP p;
+    ZigCtx z;
     GammaPrm ga, gb;
-    int phase;
-    double xa;
-    typedef ZigFast pre_t;
-    RS_DEV pre_t prefetch(u64 w) const { return p.prefetch(w); }
-    RS_DEV bool feed(u64 w, double &o) { return feed(w, prefetch(w), o); }
-    RS_DEV bool feed(u64 w, pre_t f, double &o) {
-        double r;
-        if (!p.feed(w, f, r)) return false;
-        if (phase == 0) {
-            xa = r; phase = 1; p.g = gb;
-            return false;
-        }
-        o = xa / (xa + r);
-        phase = 0; p.g = ga;
-        return true;
+    template <class S> RS_DEV double sample(S &s, Tally &t) const {
+        double x = gamma_sample(s, z, ga, t);
+        double y = gamma_sample(s, z, gb, t);
+        return x / (x + y);
     }
-    template <class TT> RS_DEV void tally(TT *t) {
-        t[0] += p.np.att; t[1] += p.np.pdf; t[4] += p.gatt;
-        p.np.att = 0; p.np.pdf = 0; p.gatt = 0;
-    }
-    RS_DEV void drop() { p.np.att = 0; p.np.pdf = 0; p.gatt = 0; }
 };
-struct DistLemire {  // bounded_uint(rng, b, 64), discrete.py:20-39: accept iff low >= (2^64-b) % b
+struct DistLemire {  // bounded_uint(rng, b, 64), discrete.py:20-39: redraw while low < (2^64-b) % b
     typedef u64 out_t;
-    typedef int pre_t;
     u64 b, thr;
-    RS_DEV pre_t prefetch(u64) const { return 0; }
-    RS_DEV bool feed(u64 w, pre_t, u64 &o) { return feed(w, o); }
-    RS_DEV bool feed(u64 w, u64 &o) {
-        u64 low = w * b;
-        if (low < thr) return false;
-        o = __umul64hi(w, b);
-        return true;
+    template <class S> RS_DEV u64 sample(S &s, Tally &) const {
+        while (true) {
+            u64 w = s.next();
+            if (w * b >= thr) return __umul64hi(w, b);
+        }
     }
-    template <class TT> RS_DEV void tally(TT *) {}
-    RS_DEV void drop() {}
-};
-struct DistRaw {
-    typedef u64 out_t;
-    RS_DEV bool feed(u64 w, u64 &o) { o = w; return true; }
-    template <class TT> RS_DEV void tally(TT *) {}
-    RS_DEV void drop() {}
-};
-struct DistU01 {
-    typedef double out_t;
-    bool fm;
-    RS_DEV bool feed(u64 w, double &o) { o = u01_of(w, fm); return true; }
-    template <class TT> RS_DEV void tally(TT *) {}
-    RS_DEV void drop() {}
+    // word-level form: every lane consumes one word per step (no divergent redraw loops)
+    RS_DEV bool accept(u64 w, u64 &o) const {
+        o = __umul64hi(w, b);
+        return w * b >= thr;
+    }
 };
 
 // ----------------------------------------------------------------------------- run writers

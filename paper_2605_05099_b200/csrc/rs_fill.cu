@@ -124,12 +124,16 @@ __device__ __forceinline__ void make_engine(const FillPlan &p, u32 t, typename E
     }
 }
 
+// The logical word stream of one segment: the buffered prefix (thread 0 of the
+// first chunk only) then the engine. `pos` is the logical position.
 template <int E>
 struct Src {
     typename EngOf<E>::type e;
     const u64 *pre;
     int npre;
+    u64 pos;
     __device__ __forceinline__ u64 next() {
+        pos++;
         if (npre > 0) { npre--; return *pre++; }
         return e.next();
     }
@@ -141,6 +145,7 @@ __device__ __forceinline__ void make_src(const FillPlan &p, u32 t, u64 pos, Src<
     make_engine<E>(p, t, s.e);
     s.npre = 0;
     s.pre = p.prefix;
+    s.pos = pos;
     u64 skip;
     if (t == 0) {
         if (pos < (u64)p.P) { s.pre = p.prefix + pos; s.npre = p.P - (int)pos; skip = 0; }
@@ -160,39 +165,33 @@ template <> struct DistOf<RS_DIST_BETA> { typedef DistBeta type; };
 template <> struct DistOf<RS_DIST_UINT64> { typedef DistLemire type; };
 
 template <int D>
+__device__ __forceinline__ void make_dist_f(const double *fp, const u64 *ip, const GammaPrm &ga, const GammaPrm &gb,
+                                            int raw, const RsZigSlow *zslow, int fm, const ZigFast *fast,
+                                            typename DistOf<D>::type &d) {
+    if constexpr (D == RS_DIST_UINT64) {
+        d.b = ip[0];
+        d.thr = ip[1];
+    } else {
+        d.z.fast = fast;
+        d.z.slow = zslow;
+        d.z.fm = fm;
+        if constexpr (D == RS_DIST_NORM) {
+            d.mu = fp[0];
+            d.sd = fp[1];
+            d.raw = raw;
+        } else if constexpr (D == RS_DIST_EXP) {
+            d.beta = fp[0];
+        } else if constexpr (D == RS_DIST_GAMMA) {
+            d.g = ga;
+        } else {
+            d.ga = ga;
+            d.gb = gb;
+        }
+    }
+}
+template <int D>
 __device__ __forceinline__ void make_dist(const FillPlan &p, const ZigFast *fast, typename DistOf<D>::type &d) {
-    if constexpr (D == RS_DIST_NORM) {
-        d.p.init(fast, p.zslow, p.fm);
-        d.mu = p.fp[0];
-        d.sd = p.fp[1];
-    } else if constexpr (D == RS_DIST_EXP) {
-        d.p.init(fast, p.zslow, p.fm);
-        d.beta = p.fp[0];
-    } else if constexpr (D == RS_DIST_GAMMA) {
-        d.p.init(fast, p.zslow, p.fm, p.ga);
-    } else if constexpr (D == RS_DIST_BETA) {
-        d.p.init(fast, p.zslow, p.fm, p.ga);
-        d.ga = p.ga; d.gb = p.gb; d.phase = 0;
-    } else {
-        d.b = p.ip[0];
-        d.thr = p.ip[1];
-    }
-}
-
-template <int D>
-__device__ __forceinline__ bool dist_feed(const FillPlan &p, typename DistOf<D>::type &d, u64 w,
-                                          typename DistOf<D>::type::out_t &o) {
-    return dist_feed<D>(p, d, w, d.prefetch(w), o);
-}
-template <int D>
-__device__ __forceinline__ bool dist_feed(const FillPlan &p, typename DistOf<D>::type &d, u64 w,
-                                          typename DistOf<D>::type::pre_t f, typename DistOf<D>::type::out_t &o) {
-    if constexpr (D == RS_DIST_NORM) {
-        if (p.raw_norm) return d.feed_raw(w, f, o);
-        return d.feed(w, f, o);
-    } else {
-        return d.feed(w, f, o);
-    }
+    make_dist_f<D>(p.fp, p.ip, p.ga, p.gb, p.raw_norm, p.zslow, p.fm, fast, d);
 }
 
 __device__ __forceinline__ void stage_tables(const FillPlan &p, ZigFast *sm) {
@@ -256,101 +255,71 @@ constexpr int minb(int E, int D) {
     return E == RS_ENG_RANLUX ? 2 : (D == RS_DIST_GAMMA || D == RS_DIST_BETA) ? 2 : D == RS_DIST_UINT64 ? 4 : 3;
 }
 
-// ----------------------------------------------------------------------------- parse loop
-// Parses from logical position `pos` (a boundary) until the first boundary at or
-// beyond `end`, or until `maxc` samples were emitted. Returns samples emitted.
-template <int E, int D, bool EMIT, class W, class TT>
-__device__ __forceinline__ u64 parse(const FillPlan &p, Src<E> &s, typename DistOf<D>::type &d, u64 &pos, u64 end,
-                                     u64 maxc, W *wr, TT *tally, u64 &last_end) {
-    typedef typename DistOf<D>::type::out_t T;
-    u64 c = 0;
-    if (maxc == 0) return 0;
-    bool boundary = true;
-    // words are generated four at a time so the engine's dependency chain overlaps the
-    // parse; words generated past the exit are simply dropped (only `pos` matters)
-    while (true) {
-        u64 w[4];
-        typename DistOf<D>::type::pre_t f[4];
-#pragma unroll
-        for (int k = 0; k < 4; k++) w[k] = s.next();
-#pragma unroll
-        for (int k = 0; k < 4; k++) f[k] = d.prefetch(w[k]);  // table loads issued together
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            if (boundary && pos >= end) return c;
-            pos++;
-            T v;
-            if (dist_feed<D>(p, d, w[k], f[k], v)) {
-                boundary = true;
-                if constexpr (EMIT) {
-                    wr->put(v);
-                    d.tally(tally);
-                    last_end = pos;
-                }
-                if (++c >= maxc) return c;
-            } else {
-                boundary = false;
-            }
-        }
-    }
-}
-
+// ----------------------------------------------------------------------------- two-pass parse
+// count: samples that START inside [seg_start, seg_end) and the exit (first sample
+// boundary at or beyond seg_end), parsing from seg_start as if it were a boundary.
 template <int E, int D>
 __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_count(const __grid_constant__ FillPlan p, u64 *cnt0, u32 *ex0) {
     __shared__ ZigFast sm[256];
     stage_tables(p, sm);
     u32 t = blockIdx.x * BLOCK + threadIdx.x;
     if (t >= p.T) return;
-    u64 pos = seg_start(p, t), end = seg_end(p, t);
+    const u64 end = seg_end(p, t);
     Src<E> s;
-    make_src<E>(p, t, pos, s);
+    make_src<E>(p, t, seg_start(p, t), s);
     typename DistOf<D>::type d;
     make_dist<D>(p, sm, d);
-    u64 dummy;
-    u64 c = parse<E, D, false, VecWriter8<u64>, u32>(p, s, d, pos, end, ~0ULL, nullptr, nullptr, dummy);
+    Tally tl;
+    u64 c = 0;
+    if constexpr (D == RS_DIST_UINT64) {  // independent one-word tokens: word-level loop
+        bool bnd = true;
+        while (!(bnd && s.pos >= end)) {
+            u64 o;
+            bnd = d.accept(s.next(), o);
+            c += bnd;
+        }
+    } else {
+        while (s.pos < end) {
+            d.sample(s, tl);
+            c++;
+        }
+    }
     cnt0[t] = c;
-    ex0[t] = (u32)(pos - end);
+    ex0[t] = (u32)(s.pos - end);
 }
 
-// lockstep convergence of the parse from entry e with the parse from entry 0
+// The true entry e of segment t is segment t-1's exit. Parse from start+e (B) and
+// from start (A) in lockstep, always advancing the one behind by one sample, until
+// they meet at a common boundary inside the segment (then counts differ only by
+// the samples before the meeting point) or B reaches its own exit.
 template <int E, int D>
 __device__ void resolve_entry(const FillPlan &p, const ZigFast *sm, u32 t, u32 e, u64 c0, u32 x0, u64 &cnt,
                               u32 &ex) {
-    u64 start = seg_start(p, t), end = seg_end(p, t);
+    const u64 start = seg_start(p, t), end = seg_end(p, t);
     Src<E> sa, sb;
     make_src<E>(p, t, start, sa);
     make_src<E>(p, t, start + e, sb);
-    typename DistOf<D>::type da, db;
-    make_dist<D>(p, sm, da);
-    make_dist<D>(p, sm, db);
-    u64 pa = start, pb = start + e;
-    bool ba = true, bb = true;
-    u64 na = 0, nb = 0;  // emissions (with start < end) before the meeting point
-    bool a_done = false;
-    typename DistOf<D>::type::out_t v;
+    typename DistOf<D>::type d;
+    make_dist<D>(p, sm, d);
+    Tally tl;
+    u64 na = 0, nb = 0;
     while (true) {
-        if (!a_done && pa == pb && ba && bb && pa < end) {  // converged inside the segment
+        if (sa.pos == sb.pos && sa.pos < end) {
             cnt = c0 - na + nb;
             ex = x0;
             return;
         }
-        if (bb && pb >= end) {  // B reached its exit without meeting A
+        if (sb.pos >= end) {
             cnt = nb;
-            ex = (u32)(pb - end);
+            ex = (u32)(sb.pos - end);
             return;
         }
-        if (!a_done && ba && pa >= end) a_done = true;
-        bool stepA = !a_done && pa < pb;
-        if (stepA) {
-            u64 w = sa.next();
-            pa++;
-            if (dist_feed<D>(p, da, w, v)) { ba = true; na++; da.drop(); }
-            else ba = false;
+        if (sa.pos < sb.pos && sa.pos < end) {
+            d.sample(sa, tl);
+            na++;
         } else {
-            u64 w = sb.next();
-            pb++;
-            if (dist_feed<D>(p, db, w, v)) { bb = true; nb++; db.drop(); }
-            else bb = false;
+            d.sample(sb, tl);
+            nb++;
         }
     }
 }
@@ -383,13 +352,15 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_fixup(const __grid_consta
     if (x != prev_ex[t]) atomicOr(&res->flag, 1u);
 }
 
+// emit: re-parse from the true entry and write this segment's samples at their
+// global offsets (exclusive scan of the counts).
 template <int E, int D>
 __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constant__ FillPlan p, const u32 *entry, const u64 *cnt,
                                                 const u64 *off, const u32 *ex, DevResult *res) {
     __shared__ ZigFast sm[256];
     stage_tables(p, sm);
     u32 t = blockIdx.x * BLOCK + threadIdx.x;
-    u32 tally[6] = {0, 0, 0, 0, 0, 0};
+    Tally tl = {0, 0, 0, 0, 0};
     if (t < p.T) {
         u64 o = off[t], c = cnt[t];
         if (t == p.T - 1) {
@@ -398,25 +369,31 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constan
         }
         if (o < p.n && c > 0) {
             u64 kmax = c < p.n - o ? c : p.n - o;
-            u64 pos = seg_start(p, t) + entry[t];
             Src<E> s;
-            make_src<E>(p, t, pos, s);
+            make_src<E>(p, t, seg_start(p, t) + entry[t], s);
             typename DistOf<D>::type d;
             make_dist<D>(p, sm, d);
             typedef typename DistOf<D>::type::out_t T;
-            VecWriter2<T> wr;
+            VecWriter8<T> wr;
             wr.init((T *)p.out, p.out0 + o);
-            u64 last_end = 0;
-            parse<E, D, true>(p, s, d, pos, ~0ULL, kmax, &wr, tally, last_end);
+            if constexpr (D == RS_DIST_UINT64) {
+                for (u64 k = 0; k < kmax;) {
+                    u64 o;
+                    if (d.accept(s.next(), o)) { wr.put(o); k++; }
+                }
+            } else {
+                for (u64 k = 0; k < kmax; k++) wr.put(d.sample(s, tl));
+            }
             wr.finish();
-            if (o + kmax == p.n) res->end_pos = last_end;
+            if (o + kmax == p.n) res->end_pos = s.pos;
         }
     }
     // tallies: warp reduce then one atomic per warp
+    u64 tv[6] = {tl.norm_att, tl.norm_pdf, tl.exp_att, tl.exp_pdf, tl.gamma_att, 0};
 #pragma unroll
-    for (int i = 0; i < 6; i++) {
-        u64 v = tally[i];
-        for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, s);  // u64: no overflow
+    for (int i = 0; i < 5; i++) {
+        u64 v = tv[i];
+        for (int sh = 16; sh > 0; sh >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, sh);
         if ((threadIdx.x & 31) == 0 && v) atomicAdd((unsigned long long *)&res->tally[i], (unsigned long long)v);
     }
 }
@@ -550,8 +527,9 @@ struct SerialSrc {
     EngSfc e, snap;
     const u64 *pre;
     int npre;
-    u64 eng;
+    u64 eng, pos;
     __device__ __forceinline__ u64 next() {
+        pos++;
         if (npre > 0) { npre--; return *pre++; }
         if (eng % CAP == 0) snap = e;
         eng++;
@@ -570,21 +548,21 @@ __global__ void k_serial(const __grid_constant__ FillPlan p, DevResult *res) {
     s.pre = p.prefix;
     s.npre = p.P;
     s.eng = 0;
-    u64 pos = 0;
-    u64 tally[6] = {0, 0, 0, 0, 0, 0};
+    s.pos = 0;
+    Tally tl = {0, 0, 0, 0, 0};
     if constexpr (D == 2) {  // u01f from halves, low half first
         float *out = (float *)p.out;
         u64 i = 0;
         if (p.pending_used) out[i++] = u01f_of(p.pending_val, p.fm);
         while (i < p.n) {
-            u64 w = s.next(); pos++;
+            u64 w = s.next();
             out[i++] = u01f_of((u32)w, p.fm);
             if (i < p.n) out[i++] = u01f_of((u32)(w >> 32), p.fm);
         }
     } else if constexpr (D == 0 || D == 1) {  // raw or power-of-two bound / u01
         u64 *out = (u64 *)p.out;
         for (u64 i = 0; i < p.n; i++) {
-            u64 w = s.next(); pos++;
+            u64 w = s.next();
             out[i] = D == 0 ? (p.ip[0] ? __umul64hi(w, p.ip[0]) : w) : bits(u01_of(w, p.fm));
         }
     } else {
@@ -593,14 +571,11 @@ __global__ void k_serial(const __grid_constant__ FillPlan p, DevResult *res) {
         make_dist<DD>(p, sm, d);
         typedef typename DistOf<DD>::type::out_t T;
         T *out = (T *)p.out;
-        for (u64 i = 0; i < p.n;) {
-            u64 w = s.next(); pos++;
-            T v;
-            if (dist_feed<DD>(p, d, w, v)) { out[i++] = v; d.tally(tally); }
-        }
+        for (u64 i = 0; i < p.n; i++) out[i] = d.sample(s, tl);
     }
-    res->end_pos = pos;
-    for (int i = 0; i < 6; i++) res->tally[i] = tally[i];
+    res->end_pos = s.pos;
+    res->tally[0] = tl.norm_att; res->tally[1] = tl.norm_pdf; res->tally[2] = tl.exp_att;
+    res->tally[3] = tl.exp_pdf; res->tally[4] = tl.gamma_att; res->tally[5] = 0;
     res->serial_consumed = s.eng;
     EngSfc f = s.snap;
     if (s.eng > 0)
@@ -685,23 +660,14 @@ __global__ void __launch_bounds__(BLOCK) k_streams(const __grid_constant__ Strea
         if (!(w[0] | w[1] | w[2] | w[3])) w[0] = 1;
         e.s0 = w[0]; e.s1 = w[1]; e.s2 = w[2]; e.s3 = w[3];
     }
-    FillPlan p;  // only the dist fields are consulted
-    p.fm = a.fm;
-    p.raw_norm = 0;
-    p.zslow = a.zslow;
-    p.fp[0] = a.fp[0]; p.fp[1] = a.fp[1]; p.fp[2] = a.fp[2]; p.fp[3] = a.fp[3];
-    p.ip[0] = a.ip[0]; p.ip[1] = a.ip[1];
-    p.ga = a.ga; p.gb = a.gb;
     typedef typename DistOf<D>::type DT;
     DT d;
-    make_dist<D>(p, sm, d);
+    make_dist_f<D>(a.fp, a.ip, a.ga, a.gb, 0, a.zslow, a.fm, sm, d);
     typedef typename DT::out_t T;
     VecWriter8<T> wr;
     wr.init((T *)a.out, j * a.nper);
-    for (u64 i = 0; i < a.nper;) {
-        T v;
-        if (dist_feed<D>(p, d, e.next(), v)) { wr.put(v); d.drop(); i++; }
-    }
+    Tally tl;
+    for (u64 i = 0; i < a.nper; i++) wr.put(d.sample(e, tl));
     wr.finish();
 }
 
