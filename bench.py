@@ -160,16 +160,11 @@ def run_ours(args, rank, world, local_rank):
     sptr = ctypes.c_void_p(stream.cuda_stream)
     peak, peak_src = measured_peaks()
 
-    def slice_stream(dist_name, words_per_rank):
-        r = state_io.create("philox", seed=[7])
-        r.set_full_mantissa(True)
-        st = r.get_state()
-        st[0] = (st[0] + rank * (words_per_rank // 4)) & (2 ** 64 - 1)
-        r.set_state(st)
-        return r
+    from paper_2605_05099_b200 import shard
 
-    r64 = slice_stream("u01", N_HEAD)
-    r32 = slice_stream("u01f", N_HEAD // 2)
+    # rank g fills words [g*W, (g+1)*W) of the one logical stream (counter offset, no collective)
+    r64 = shard.shard_rng("philox", [7], rank, N_HEAD, full_mantissa=True)
+    r32 = shard.shard_rng("philox", [7], rank, N_HEAD // 2, full_mantissa=True)
     s64, s32 = r64.to_stream(), r32.to_stream()
     out64 = torch.empty(N_HEAD, dtype=torch.float64, device=dev)
     out32 = torch.empty(N_HEAD, dtype=torch.float32, device=dev)
@@ -263,6 +258,17 @@ def run_ours(args, rank, world, local_rank):
     if world == 1 and not args.no_per_config:
         per_config = run_per_config(dev, stream, sptr, out64, peak)
 
+    traffic, limiter = None, None
+    prof = os.path.join(ROOT, "profiles", "r01_ncu_philox_u01_f64.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            pj = json.load(f)
+        traffic = pj.get("traffic_bytes_per_launch")
+        heavy = pj["metrics"].get("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed", {}).get("value")
+        if heavy:
+            limiter = ("integer multiply: Philox-4x64-10 needs 80 IMAD.WIDE.U32 per 4-word block; ncu: fmaheavy "
+                       "pipe %.1f%% busy, DRAM %.1f%% (profiles/r01_ncu_philox_u01_f64.json)" % (
+                           heavy, pj["metrics"]["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]["value"]))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -272,8 +278,9 @@ def run_ours(args, rank, world, local_rank):
                                "+ u01f f32 n=2^30 per GPU; rank g = counter-offset slice g",
                    "l2": "outputs 12 GiB per step >> 126 MB L2 (inputs larger than L2, no flush)",
                    "parallelism": "dp%d (independent counter slices, no collective)" % world},
-        "roofline": {"bound": "hbm", "kernel": "k_fixed<philox,u01> (u01 f64 fill)", "achieved": achieved,
-                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+        "roofline": {"bound": "hbm", "kernel": "k_philox_fixed<FX_U01> (u01 f64 fill)", "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per launch (ncu --set full, same kernel)", "limiter": limiter,
                      "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes64,
                      "avg_launch_ms": avg64, "u01f_f32_launch_ms": avg32,
                      "u01f_f32_achieved_gbs": 4.0 * N_HEAD / (avg32 / 1e3) / 1e9},

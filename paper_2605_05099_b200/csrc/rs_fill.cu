@@ -667,7 +667,14 @@ __global__ void __launch_bounds__(BLOCK) k_streams(const __grid_constant__ Strea
     VecWriter8<T> wr;
     wr.init((T *)a.out, j * a.nper);
     Tally tl;
-    for (u64 i = 0; i < a.nper; i++) wr.put(d.sample(e, tl));
+    if constexpr (D == RS_DIST_UINT64) {
+        for (u64 i = 0; i < a.nper;) {
+            u64 o;
+            if (d.accept(e.next(), o)) { wr.put(o); i++; }
+        }
+    } else {
+        for (u64 i = 0; i < a.nper; i++) wr.put(d.sample(e, tl));
+    }
     wr.finish();
 }
 
