@@ -414,26 +414,76 @@ __device__ __forceinline__ u64 fx_map(const FillPlan &p, u64 w) {
 
 // u64/f64 outputs: logical word i -> out[i]. u01f: logical word i -> f32 out[pp + 2i], out[pp + 2i + 1]
 // (written as one 8-byte element when that address is 8-byte aligned, else as two scalars).
+// out[i] = map(word i) for i in [first, last). Each lane owns a contiguous run,
+// so direct stores from a warp would touch 32 different lines. Instead lanes
+// write 16-word chunks (one 128-byte line each) into a padded per-warp shared tile
+// (row stride 17 words: conflict-free), and the warp then stores 4 whole lines per
+// STG.128 instruction. The ragged head (up to line alignment, and the buffered
+// prefix) and tail are scalar.
+constexpr int FX_ROW = 17;
+template <int E, int MODE>
+__device__ __forceinline__ void write_run(const FillPlan &p, Src<E> &s, u64 *out, u64 first, u64 last,
+                                          u64 (*tile)[FX_ROW], bool active) {
+    const u32 lane = threadIdx.x & 31;
+    u64 i = first;
+    if (active)
+        while (i < last && ((((uintptr_t)(out + i)) & 127) != 0 || s.npre > 0)) out[i++] = fx_map<MODE>(p, s.next());
+    u64 nchunk = active && last > i ? (last - i) / 16 : 0;
+    u64 maxc = nchunk;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        u64 v = __shfl_xor_sync(0xFFFFFFFFu, maxc, o);
+        maxc = v > maxc ? v : maxc;
+    }
+    for (u64 k = 0; k < maxc; k++) {
+        bool has = k < nchunk;
+        if (has) {
+            if constexpr (E == RS_ENG_RANLUX) {  // keep the 9x9-limb mulmod out of an unrolled body (I-cache)
+#pragma unroll 1
+                for (int j = 0; j < 16; j++) tile[lane][j] = fx_map<MODE>(p, s.e.next());
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; j++) tile[lane][j] = fx_map<MODE>(p, s.e.next());
+            }
+        }
+        u64 dst = has ? (u64)(uintptr_t)(out + i) : 0;
+        __syncwarp();
+#pragma unroll
+        for (int g = 0; g < 8; g++) {  // 4 rows (lines) per instruction, 8 lanes x 16 B per row
+            u32 r = 4 * g + (lane >> 3), c = lane & 7;
+            u64 d = __shfl_sync(0xFFFFFFFFu, dst, r);
+            if (d) {
+                u64 x = tile[r][2 * c], y = tile[r][2 * c + 1];
+                asm volatile("st.global.v2.b64 [%0], {%1, %2};" ::"l"(d + 16 * c), "l"(x), "l"(y) : "memory");
+            }
+        }
+        __syncwarp();
+        if (has) i += 16;
+    }
+    if (active)
+        for (; i < last; i++) out[i] = fx_map<MODE>(p, s.e.next());
+}
+
 template <int E, int MODE>
 __global__ void __launch_bounds__(BLOCK) k_fixed(const __grid_constant__ FillPlan p) {
+    __shared__ u64 tiles[BLOCK / 32][32][FX_ROW];
+    u64 (*tile)[FX_ROW] = tiles[threadIdx.x >> 5];
     u32 t = blockIdx.x * BLOCK + threadIdx.x;
-    if (t >= p.T) return;
+    // every lane of a warp takes part in the tile stores; idle lanes just contribute nothing
+    bool active = t < p.T && ((u64)t * p.L < p.weng || t == 0);
     u64 j0 = (u64)t * p.L;
-    if (j0 >= p.weng && t != 0) return;
     u64 j1 = j0 + p.L < p.weng ? j0 + p.L : p.weng;
+    if (j1 < j0) j1 = j0;
     u64 first = t == 0 ? 0 : (u64)p.P + j0;       // first logical word
     u64 last = (u64)p.P + j1;                     // one past
     Src<E> s;
-    make_engine<E>(p, t, s.e);
+    if (t < p.T) make_engine<E>(p, t, s.e);
     s.pre = p.prefix;
     s.npre = t == 0 ? p.P : 0;
     if constexpr (MODE != FX_U01F) {
         u64 *out = (u64 *)p.out;
         if (t == 0 && last > p.n) last = p.n;  // n < P: prefix only
-        VecWriter8<u64> wr;
-        wr.init(out, first);
-        for (u64 i = first; i < last; i++) wr.put(fx_map<MODE>(p, s.next()));
-        wr.finish();
+        write_run<E, MODE>(p, s, out, first, last, tile, active);
     } else {
         float *out = (float *)p.out;
         u64 halves = p.n - p.pending_used;  // halves to emit
@@ -441,19 +491,16 @@ __global__ void __launch_bounds__(BLOCK) k_fixed(const __grid_constant__ FillPla
         u64 full_words = halves / 2;        // words whose both halves are emitted
         u64 lim = last < full_words ? last : full_words;
         float *o2 = out + p.pending_used;
-        if ((((uintptr_t)o2) & 7) == 0) {
-            VecWriter8<u64> wr;
-            wr.init((u64 *)o2, first);
-            for (u64 i = first; i < lim; i++) wr.put(fx_map<MODE>(p, s.next()));
-            wr.finish();
-        } else {
+        if ((((uintptr_t)o2) & 7) == 0) {  // warp-uniform: the whole grid shares o2
+            write_run<E, MODE>(p, s, (u64 *)o2, first, lim > first ? lim : first, tile, active);
+        } else if (active) {
             for (u64 i = first; i < lim; i++) {
                 u64 w = s.next();
                 o2[2 * i] = u01f_of((u32)w, p.fm);
                 o2[2 * i + 1] = u01f_of((u32)(w >> 32), p.fm);
             }
         }
-        if ((halves & 1) && full_words >= first && full_words < last) {  // trailing low half
+        if (active && (halves & 1) && full_words >= first && full_words < last) {  // trailing low half
             u64 w = 0;
             for (u64 i = lim; i <= full_words; i++) w = s.next();
             o2[2 * full_words] = u01f_of((u32)w, p.fm);
@@ -483,36 +530,46 @@ __global__ void __launch_bounds__(BLOCK) k_philox_fixed(const __grid_constant__ 
             for (int i = 0; i < p.P && (u64)i < p.n; i++) out[i] = fx_map<MODE>(p, p.prefix[i]);
         }
     }
-    for (; b < nblk; b += stride) {
-        u64 c0 = p.base[0] + b, c1 = p.base[1], c2 = p.base[2], c3 = p.base[3];
-        if (c0 < b) { if (++c1 == 0) { if (++c2 == 0) ++c3; } }
-        u64 w0, w1, w2, w3;
-        philox4x64_10_rk<V>(c0, c1, c2, c3, p.rk0, p.rk1, w0, w1, w2, w3);
-        if constexpr (MODE == FX_U01F) {
-            u64 f = (u64)p.pending_used + 2ULL * ((u64)p.P + 4 * b);  // first f32 index of this block
-            u64 q0 = fx_map<MODE>(p, w0), q1 = fx_map<MODE>(p, w1), q2 = fx_map<MODE>(p, w2), q3 = fx_map<MODE>(p, w3);
-            float *out = (float *)p.out;
-            if (p.vec_ok && f + 8 <= p.n) {
-                asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(out + f), "l"(q0), "l"(q1), "l"(q2),
-                             "l"(q3) : "memory");
-            } else {
-                u64 q[4] = {q0, q1, q2, q3};
+    // two independent blocks per iteration (ILP for the IMAD pipe)
+    for (; b < nblk; b += 2 * stride) {
+        u64 w[2][4];
 #pragma unroll
-                for (int i = 0; i < 8; i++)
-                    if (f + i < p.n) out[f + i] = __uint_as_float((u32)(q[i >> 1] >> (32 * (i & 1))));
-            }
-        } else {
-            u64 e = (u64)p.P + 4 * b;
-            u64 q0 = fx_map<MODE>(p, w0), q1 = fx_map<MODE>(p, w1), q2 = fx_map<MODE>(p, w2), q3 = fx_map<MODE>(p, w3);
-            u64 *out = (u64 *)p.out;
-            if (p.vec_ok && e + 4 <= p.n) {
-                asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(out + e), "l"(q0), "l"(q1), "l"(q2),
-                             "l"(q3) : "memory");
+        for (int h = 0; h < 2; h++) {
+            u64 bb = b + h * stride;
+            u64 c0 = p.base[0] + bb, c1 = p.base[1], c2 = p.base[2], c3 = p.base[3];
+            if (c0 < bb) { if (++c1 == 0) { if (++c2 == 0) ++c3; } }
+            philox4x64_10_rk<V>(c0, c1, c2, c3, p.rk0, p.rk1, w[h][0], w[h][1], w[h][2], w[h][3]);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            u64 bb = b + h * stride;
+            if (bb >= nblk) break;
+            u64 q0 = fx_map<MODE>(p, w[h][0]), q1 = fx_map<MODE>(p, w[h][1]);
+            u64 q2 = fx_map<MODE>(p, w[h][2]), q3 = fx_map<MODE>(p, w[h][3]);
+            if constexpr (MODE == FX_U01F) {
+                u64 f = (u64)p.pending_used + 2ULL * ((u64)p.P + 4 * bb);  // first f32 index of this block
+                float *out = (float *)p.out;
+                if (p.vec_ok && f + 8 <= p.n) {
+                    asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(out + f), "l"(q0), "l"(q1),
+                                 "l"(q2), "l"(q3) : "memory");
+                } else {
+                    u64 q[4] = {q0, q1, q2, q3};
+#pragma unroll
+                    for (int i = 0; i < 8; i++)
+                        if (f + i < p.n) out[f + i] = __uint_as_float((u32)(q[i >> 1] >> (32 * (i & 1))));
+                }
             } else {
-                if (e < p.n) out[e] = q0;
-                if (e + 1 < p.n) out[e + 1] = q1;
-                if (e + 2 < p.n) out[e + 2] = q2;
-                if (e + 3 < p.n) out[e + 3] = q3;
+                u64 e = (u64)p.P + 4 * bb;
+                u64 *out = (u64 *)p.out;
+                if (p.vec_ok && e + 4 <= p.n) {
+                    asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(out + e), "l"(q0), "l"(q1),
+                                 "l"(q2), "l"(q3) : "memory");
+                } else {
+                    if (e < p.n) out[e] = q0;
+                    if (e + 1 < p.n) out[e + 1] = q1;
+                    if (e + 2 < p.n) out[e + 2] = q2;
+                    if (e + 3 < p.n) out[e + 3] = q3;
+                }
             }
         }
     }
