@@ -75,7 +75,26 @@ typedef enum {
     RS_DIST_EXP = 5,     /* "exp"   : fparams {beta} */
     RS_DIST_GAMMA = 6,   /* "gamma" : fparams {alpha, theta} */
     RS_DIST_BETA = 7,    /* "beta"  : fparams {a, b} */
-    RS_DIST_STDNORM = 8  /* std_norm without the norm epilogue (the mvn z draws, continuous.py:332) */
+    RS_DIST_STDNORM = 8, /* std_norm without the norm epilogue (the mvn z draws, continuous.py:332) */
+    /* derived laws and transforms (continuous.py:136-290), bit-exact to the reference's
+       bitexact mode (det_exp/det_log); within 4 ulp of its default numpy-vectorised mode */
+    RS_DIST_UNIF = 9,         /* {a, b}                      f64 */
+    RS_DIST_UNIFF = 10,       /* {a, b}                      f32, 32-bit halves */
+    RS_DIST_NORMF = 11,       /* {mu, var}                   f32, 32-bit halves */
+    RS_DIST_EXPF = 12,        /* {beta}                      f32, 32-bit halves */
+    RS_DIST_LOGNORMAL = 13,   /* {mu, var} */
+    RS_DIST_CHI2 = 14,        /* {nu} */
+    RS_DIST_T = 15,           /* {nu} */
+    RS_DIST_F = 16,           /* {nu1, nu2} */
+    RS_DIST_GUMBEL = 17,      /* {mu, beta} */
+    RS_DIST_PARETO = 18,      /* {alpha, xm} */
+    RS_DIST_GPD = 19,         /* {xi, mu, sigma} */
+    RS_DIST_WEIBULL = 20,     /* {k, lam} */
+    RS_DIST_SKEW_NORMAL = 21, /* {alpha, mu, sigma} */
+    /* integers (discrete.py:20-55): */
+    RS_DIST_UINT32 = 22,      /* "uint8|16|32": iparams {b, width}           -> u32 on 32-bit halves */
+    RS_DIST_INT32 = 23,       /* "int": iparams {span, 32, m, full_span}      -> i32 on 32-bit halves */
+    RS_DIST_INT64 = 24        /* "long_long": iparams {span, 64, m, full_span} -> i64 */
 } rs_dist;
 
 /* A generator's full logical position (engine words + WordBuffer, buffer.py:17-60).

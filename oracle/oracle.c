@@ -38,7 +38,9 @@ enum { E_X256PP = 1, E_X256SS = 2, E_PCG64 = 5, E_PHILOX = 6, E_SFC64 = 8, E_RAN
 
 /* distribution ids, shared with include/randstream_b200.h */
 enum { D_UINT64 = 1, D_U01 = 2, D_U01F = 3, D_NORM = 4, D_EXP = 5, D_GAMMA = 6, D_BETA = 7,
-       D_STDNORM = 8 };
+       D_STDNORM = 8, D_UNIF = 9, D_UNIFF = 10, D_NORMF = 11, D_EXPF = 12, D_LOGNORMAL = 13, D_CHI2 = 14,
+       D_T = 15, D_F = 16, D_GUMBEL = 17, D_PARETO = 18, D_GPD = 19, D_WEIBULL = 20, D_SKEW_NORMAL = 21,
+       D_UINT32 = 22, D_INT32 = 23, D_INT64 = 24 };
 
 typedef struct orc_rng {
     int eid;
@@ -553,6 +555,65 @@ static double gamma_s(orc_rng *r, double alpha, double theta) {
     }
 }
 
+
+static double to_f32(double x) { return (double)(float)x; }  /* numpy float32 rounding (_f32) */
+
+/* std_norm_f, src/continuous.py:96-115 (32-bit halves, f32 tables) */
+static double std_norm_f(orc_rng *r) {
+    const double nor_r = d_from_bits(RS_NOR_R_BITS), nor_inv_r = d_from_bits(RS_NOR_INV_R_BITS);
+    for (;;) {
+        uint32_t w = take_u32(r);
+        int idx = (int)(w & 0xFF);
+        int sign = (int)((w >> 8) & 1);
+        uint32_t rabs = (w >> 9) & 0x7FFFFF;
+        float wf; memcpy(&wf, &RS_WI_F_BITS[idx], 4);
+        double x = to_f32((double)rabs * (double)wf);
+        if (rabs < RS_KI_F[idx]) return sign ? -x : x;
+        if (idx == 0) {
+            for (;;) {
+                double xx = -nor_inv_r * orc_det_log(1.0 - u01f(r));
+                double yy = -orc_det_log(1.0 - u01f(r));
+                if (yy + yy > xx * xx) { double t = to_f32(nor_r + xx); return sign ? -t : t; }
+            }
+        }
+        double u = (double)(take_u32(r) >> 8) * 5.9604644775390625e-08;
+        float fi, fim1; memcpy(&fi, &RS_FI_F_BITS[idx], 4); memcpy(&fim1, &RS_FI_F_BITS[idx - 1], 4);
+        double y = (double)fi + u * ((double)fim1 - (double)fi);
+        if (y < orc_det_exp(-0.5 * x * x)) return sign ? -x : x;
+    }
+}
+/* std_exp_f, src/continuous.py:118-133 */
+static double std_exp_f(orc_rng *r) {
+    const double exp_r = d_from_bits(RS_EXP_R_BITS);
+    for (;;) {
+        uint32_t w = take_u32(r);
+        int idx = (int)(w & 0xFF);
+        uint32_t rabs = (w >> 8) & 0xFFFFFF;
+        float wf; memcpy(&wf, &RS_WE_F_BITS[idx], 4);
+        double x = to_f32((double)rabs * (double)wf);
+        if (rabs < RS_KE_F[idx]) return x;
+        if (idx == 0) return to_f32(exp_r - orc_det_log(1.0 - u01f(r)));
+        double u = (double)(take_u32(r) >> 8) * 5.9604644775390625e-08;
+        float fe, fem1; memcpy(&fe, &RS_FE_F_BITS[idx], 4); memcpy(&fem1, &RS_FE_F_BITS[idx - 1], 4);
+        double y = (double)fe + u * ((double)fem1 - (double)fe);
+        if (y < orc_det_exp(-x)) return x;
+    }
+}
+
+/* bounded_uint for widths 8/16/32 on 32-bit halves, src/discrete.py:14-39 */
+static uint64_t bounded32(orc_rng *r, uint64_t b, int width) {
+    uint64_t mask = (width == 32) ? 0xFFFFFFFFULL : ((1ULL << width) - 1);
+    uint64_t x = take_u32(r) & mask;
+    if (b == 0) return x;
+    uint64_t m = x * b;
+    uint64_t low = m & mask;
+    if (low < b) {
+        uint64_t thr = ((1ULL << width) - b) % b;
+        while (low < thr) { x = take_u32(r) & mask; m = x * b; low = m & mask; }
+    }
+    return m >> width;
+}
+
 /* bounded_uint width 64, src/discrete.py:20-39; b_is_2p64 covers b == 2^64 */
 static uint64_t bounded64(orc_rng *r, uint64_t b, int b_is_2p64) {
     uint64_t x = take_u64(r);
@@ -604,6 +665,83 @@ int orc_fill(orc_rng *r, int dist, const double *fp, const uint64_t *ip, uint64_
             od[i] = x / (x + y);
         }
         return 0;
+    /* derived laws and transforms, src/continuous.py:136-290 (bitexact forms) */
+    case D_UNIF: for (uint64_t i = 0; i < n; i++) od[i] = fp[0] + u01(r) * (fp[1] - fp[0]); return 0;
+    case D_UNIFF: for (uint64_t i = 0; i < n; i++) of[i] = (float)(fp[0] + u01f(r) * (fp[1] - fp[0])); return 0;
+    case D_NORMF: {
+        double sd = sqrt(fp[1]);
+        for (uint64_t i = 0; i < n; i++) of[i] = (float)(fp[0] + sd * std_norm_f(r));
+        return 0;
+    }
+    case D_EXPF: for (uint64_t i = 0; i < n; i++) of[i] = (float)(fp[0] * std_exp_f(r)); return 0;
+    case D_LOGNORMAL: {
+        double sd = sqrt(fp[1]);
+        for (uint64_t i = 0; i < n; i++) od[i] = orc_det_exp(fp[0] + sd * std_norm(r));
+        return 0;
+    }
+    case D_CHI2: for (uint64_t i = 0; i < n; i++) od[i] = gamma_s(r, fp[0] / 2.0, 2.0); return 0;
+    case D_T:
+        for (uint64_t i = 0; i < n; i++) {
+            double z = std_norm(r);
+            double v = gamma_s(r, fp[0] / 2.0, 2.0);
+            od[i] = z / sqrt(v / fp[0]);
+        }
+        return 0;
+    case D_F:
+        for (uint64_t i = 0; i < n; i++) {
+            double x = gamma_s(r, fp[0] / 2.0, 1.0);
+            double y = gamma_s(r, fp[1] / 2.0, 1.0);
+            od[i] = (x / fp[0]) / (y / fp[1]);
+        }
+        return 0;
+    case D_GUMBEL:
+        for (uint64_t i = 0; i < n; i++) od[i] = fp[0] - fp[1] * orc_det_log(-orc_det_log(u01(r)));
+        return 0;
+    case D_PARETO: for (uint64_t i = 0; i < n; i++) od[i] = fp[1] * orc_det_exp(std_exp(r) / fp[0]); return 0;
+    case D_GPD:
+        for (uint64_t i = 0; i < n; i++) {
+            double xi = fp[0], mu = fp[1], sigma = fp[2];
+            if (xi == 0.0) { od[i] = mu + sigma * std_exp(r); continue; }
+            double pp = orc_det_exp(std_exp(r) * fabs(xi));
+            od[i] = xi > 0.0 ? mu + sigma * (pp - 1.0) / xi : mu - sigma * (1.0 - 1.0 / pp) / xi;
+        }
+        return 0;
+    case D_WEIBULL:
+        for (uint64_t i = 0; i < n; i++) od[i] = fp[1] * orc_det_exp(orc_det_log(std_exp(r)) / fp[0]);
+        return 0;
+    case D_SKEW_NORMAL: {
+        double alpha = fp[0], mu = fp[1], sigma = fp[2];
+        double delta = alpha / sqrt(1.0 + alpha * alpha);
+        double cd = sqrt(1.0 - delta * delta);
+        for (uint64_t i = 0; i < n; i++) {
+            double z1 = std_norm(r);
+            double z2 = std_norm(r);
+            od[i] = mu + sigma * (delta * fabs(z1) + cd * z2);
+        }
+        return 0;
+    }
+    /* bounded integers on halves / signed ranges, src/discrete.py:20-55,103-118.
+       ip = {b or span, width, m (two's complement), full_span_flag} */
+    case D_UINT32: {
+        uint32_t *o32 = (uint32_t *)out;
+        for (uint64_t i = 0; i < n; i++) o32[i] = (uint32_t)bounded32(r, ip[0], (int)ip[1]);
+        return 0;
+    }
+    case D_INT32: {
+        int32_t *o = (int32_t *)out;
+        for (uint64_t i = 0; i < n; i++) {
+            uint64_t v = ip[3] ? (uint64_t)take_u32(r) : bounded32(r, ip[0], 32);
+            o[i] = (int32_t)(uint32_t)((uint32_t)ip[2] + (uint32_t)v);
+        }
+        return 0;
+    }
+    case D_INT64: {
+        for (uint64_t i = 0; i < n; i++) {
+            uint64_t v = ip[3] ? take_u64(r) : bounded64(r, ip[0], 0);
+            o64[i] = ip[2] + v;
+        }
+        return 0;
+    }
     }
     return -1;
 }

@@ -24,7 +24,11 @@ LIB_PATH = HERE / "liboracle.so"
 
 ENGINE_IDS = {"x256++": 1, "x256**": 2, "pcg64": 5, "philox": 6, "sfc64": 8, "ranlux++": 10}
 STATE_WORDS = {1: 4, 2: 4, 5: 4, 6: 6, 8: 4, 10: 9}
-DIST_IDS = {"uint64": 1, "u01": 2, "u01f": 3, "norm": 4, "exp": 5, "gamma": 6, "beta": 7, "stdnorm": 8}
+DIST_IDS = {"uint64": 1, "u01": 2, "u01f": 3, "norm": 4, "exp": 5, "gamma": 6, "beta": 7, "stdnorm": 8,
+            "unif": 9, "uniff": 10, "normf": 11, "expf": 12, "lognormal": 13, "chi2": 14, "t": 15, "f": 16,
+            "gumbel": 17, "pareto": 18, "gpd": 19, "weibull": 20, "skew_normal": 21,
+            "uint8": 22, "uint16": 22, "uint32": 22, "int": 23, "long_long": 24}
+F32_DISTS = ("u01f", "uniff", "normf", "expf")
 TALLY_NAMES = ("norm", "exp", "gamma")
 CAP = 144
 
@@ -104,7 +108,30 @@ def fparams_for(dist, params):
         return [float(p["alpha"]), float(p.get("theta", 1.0)), 0.0, 0.0]
     if dist == "beta":
         return [float(p["a"]), float(p["b"]), 0.0, 0.0]
+    if dist in ("unif", "uniff"):
+        return [float(p.get("a", 0.0)), float(p.get("b", 1.0)), 0.0, 0.0]
+    if dist in ("normf", "lognormal"):
+        return [float(p.get("mu", 0.0)), float(p.get("var", 1.0)), 0.0, 0.0]
+    if dist == "expf":
+        return [float(p.get("beta", 1.0)), 0.0, 0.0, 0.0]
+    if dist in ("chi2", "t"):
+        return [float(p["nu"]), 0.0, 0.0, 0.0]
+    if dist == "f":
+        return [float(p["nu1"]), float(p["nu2"]), 0.0, 0.0]
+    if dist == "gumbel":
+        return [float(p.get("mu", 0.0)), float(p.get("beta", 1.0)), 0.0, 0.0]
+    if dist == "pareto":
+        return [float(p["alpha"]), float(p.get("xm", 1.0)), 0.0, 0.0]
+    if dist == "gpd":
+        return [float(p["xi"]), float(p.get("mu", 0.0)), float(p.get("sigma", 1.0)), 0.0]
+    if dist == "weibull":
+        return [float(p["k"]), float(p.get("lam", 1.0)), 0.0, 0.0]
+    if dist == "skew_normal":
+        return [float(p.get("alpha", 0.0)), float(p.get("mu", 0.0)), float(p.get("sigma", 1.0)), 0.0]
     return [0.0, 0.0, 0.0, 0.0]
+
+
+WIDTH = {"uint8": 8, "uint16": 16, "uint32": 32}
 
 
 def iparams_for(dist, params):
@@ -114,14 +141,29 @@ def iparams_for(dist, params):
         if b == 1 << 64:
             return [0, 1, 0, 0]
         return [b, 0, 0, 0]
+    if dist in WIDTH:
+        return [int(p.get("b", 0)), WIDTH[dist], 0, 0]
+    if dist in ("int", "long_long"):
+        w = 32 if dist == "int" else 64
+        half = 1 << (w - 1)
+        m, hi = int(p.get("m", -half)), int(p.get("n", half - 1))
+        span = hi - m + 1
+        full = 1 if span == 1 << w else 0
+        return [0 if full else span, w, m & 0xFFFFFFFFFFFFFFFF, full]
     return [0, 0, 0, 0]
 
 
 def out_dtype(dist):
     if dist == "uint64":
         return np.uint64
-    if dist == "u01f":
+    if dist in F32_DISTS:
         return np.float32
+    if dist in WIDTH:
+        return np.uint32
+    if dist == "int":
+        return np.int32
+    if dist == "long_long":
+        return np.int64
     return np.float64
 
 

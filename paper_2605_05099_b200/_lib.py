@@ -15,7 +15,10 @@ CAP = 144
 
 RS_OK, RS_ERR_VALUE, RS_ERR_UNSUPPORTED, RS_ERR_CUDA, RS_ERR_INTERNAL = range(5)
 
-DIST_IDS = {"uint64": 1, "u01": 2, "u01f": 3, "norm": 4, "exp": 5, "gamma": 6, "beta": 7, "stdnorm": 8}
+DIST_IDS = {"uint64": 1, "u01": 2, "u01f": 3, "norm": 4, "exp": 5, "gamma": 6, "beta": 7, "stdnorm": 8,
+            "unif": 9, "uniff": 10, "normf": 11, "expf": 12, "lognormal": 13, "chi2": 14, "t": 15, "f": 16,
+            "gumbel": 17, "pareto": 18, "gpd": 19, "weibull": 20, "skew_normal": 21,
+            "uint8": 22, "uint16": 22, "uint32": 22, "int": 23, "long_long": 24}
 
 U64P = ctypes.POINTER(ctypes.c_uint64)
 DBLP = ctypes.POINTER(ctypes.c_double)

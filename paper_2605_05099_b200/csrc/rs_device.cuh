@@ -544,54 +544,187 @@ RS_DEV double gamma_sample(S &s, const ZigCtx &z, const GammaPrm &g, Tally &t) {
     return g.theta * r * det_exp_dev(det_log_dev(u) / g.alpha);
 }
 
-// ----------------------------------------------------------------------------- distributions
-// A Dist draws one sample per call to sample(s, t).
+// f32 ziggurats on 32-bit halves (continuous.py:96-133): strips {K (u32), W (f32)}
+struct ZigFastF {
+    u32 k;
+    float w;
+};
+struct RsZigSlowF {
+    float f[256];
+};
+struct ZigCtxF {
+    const ZigFastF *fast;  // shared memory
+    const RsZigSlowF *slow;
+    bool fm;
+};
+RS_DEV double f32r(double x) { return (double)__double2float_rn(x); }  // numpy float32(), _f32
 
-struct DistNorm {  // norm: float(mu) + sqrt(var) * z (continuous.py:157-158); raw = std_norm (mvn z)
+template <class S>
+RS_DEV double std_norm_f(S &s, const ZigCtxF &z) {
+    while (true) {
+        u32 w = s.next32();
+        int idx = (int)(w & 0xFF);
+        u32 rabs = (w >> 9) & 0x7FFFFFu;
+        ZigFastF f = z.fast[idx];
+        double x = f32r((double)rabs * (double)f.w);
+        bool neg = (w >> 8) & 1;
+        if (rabs < f.k) return neg ? -x : x;
+        if (idx == 0) {
+            while (true) {
+                double xx = -dbl(RS_NOR_INV_R_BITS) * det_log_dev(1.0 - (double)u01f_of(s.next32(), z.fm));
+                double yy = -det_log_dev(1.0 - (double)u01f_of(s.next32(), z.fm));
+                if (yy + yy > xx * xx) {
+                    double t = f32r(dbl(RS_NOR_R_BITS) + xx);
+                    return neg ? -t : t;
+                }
+            }
+        }
+        double u = (double)(s.next32() >> 8) * 5.9604644775390625e-08;
+        double fi = (double)__ldg(&z.slow->f[idx]), fim1 = (double)__ldg(&z.slow->f[idx - 1]);
+        double y = fi + u * (fim1 - fi);
+        if (y < det_exp_dev(-0.5 * x * x)) return neg ? -x : x;
+    }
+}
+
+template <class S>
+RS_DEV double std_exp_f(S &s, const ZigCtxF &z) {
+    while (true) {
+        u32 w = s.next32();
+        int idx = (int)(w & 0xFF);
+        u32 rabs = (w >> 8) & 0xFFFFFFu;
+        ZigFastF f = z.fast[idx];
+        double x = f32r((double)rabs * (double)f.w);
+        if (rabs < f.k) return x;
+        if (idx == 0) return f32r(dbl(RS_EXP_R_BITS) - det_log_dev(1.0 - (double)u01f_of(s.next32(), z.fm)));
+        double u = (double)(s.next32() >> 8) * 5.9604644775390625e-08;
+        double fe = (double)__ldg(&z.slow->f[idx]), fem1 = (double)__ldg(&z.slow->f[idx - 1]);
+        double y = fe + u * (fem1 - fe);
+        if (y < det_exp_dev(-x)) return x;
+    }
+}
+
+// ----------------------------------------------------------------------------- distributions
+// A Dist draws one sample per call to sample(s, t). Families share a kernel and pick
+// the law with a (warp-uniform) kind, which keeps the number of kernel instantiations
+// small. HALF marks samplers fed by 32-bit halves (stream positions in halves).
+
+enum { NK_NORM = 0, NK_STD = 1, NK_LOGNORMAL = 2, NK_SKEW = 3 };
+struct DistNorm {  // continuous.py:157-158 (norm), :176-177 (lognormal), :281-290 (skew_normal), mvn z
     typedef double out_t;
+    static constexpr bool HALF = false;
     ZigCtx z;
-    double mu, sd;
-    int raw;
+    double a, b, c, d;  // NORM/LOGNORMAL: mu, sd | SKEW: delta, sqrt(1-delta^2), mu, sigma
+    int kind;
+    // a skew-normal sample is a pair of normals: the phase-1 parse starts with its second one
+    RS_DEV bool paired() const { return kind == NK_SKEW; }
+    template <class S> RS_DEV void skip_second(S &s, Tally &t) const { std_norm(s, z, t); }
     template <class S> RS_DEV double sample(S &s, Tally &t) const {
         double v = std_norm(s, z, t);
-        return raw ? v : mu + sd * v;
+        if (kind == NK_STD) return v;
+        if (kind == NK_SKEW) {
+            double v2 = std_norm(s, z, t);
+            return c + d * (a * fabs(v) + b * v2);
+        }
+        double r = a + b * v;
+        return kind == NK_LOGNORMAL ? det_exp_dev(r) : r;
     }
 };
-struct DistExp {  // beta * std_exp (continuous.py:165-169)
+enum { EK_EXP = 0, EK_PARETO = 1, EK_GPD = 2, EK_WEIBULL = 3 };
+struct DistExp {  // continuous.py:165-169 (exp), :252-254 (pareto), :257-266 (gpd), :269-274 (weibull)
     typedef double out_t;
+    static constexpr bool HALF = false;
     ZigCtx z;
-    double beta;
-    template <class S> RS_DEV double sample(S &s, Tally &t) const { return beta * std_exp(s, z, t); }
+    double a, b, c;  // EXP: beta | PARETO: alpha, xm | GPD: xi, mu, sigma | WEIBULL: k, lam
+    int kind;
+    RS_DEV bool paired() const { return false; }
+    template <class S> RS_DEV void skip_second(S &, Tally &) const {}
+    template <class S> RS_DEV double sample(S &s, Tally &t) const {
+        double e = std_exp(s, z, t);
+        if (kind == EK_EXP) return a * e;
+        if (kind == EK_PARETO) return b * det_exp_dev(e / a);
+        if (kind == EK_WEIBULL) return b * det_exp_dev(det_log_dev(e) / a);
+        if (a == 0.0) return b + c * e;  // gpd, xi == 0
+        double p = det_exp_dev(e * fabs(a));
+        return a > 0.0 ? b + c * (p - 1.0) / a : b - c * (1.0 - 1.0 / p) / a;
+    }
 };
-struct DistGamma {
+enum { GK_GAMMA = 0, GK_BETA = 1, GK_T = 2, GK_F = 3 };
+struct DistGamma {  // continuous.py:183-212 (gamma, chi2 = gamma(nu/2, 2)), :215-218 beta, :228-234 t, :237-243 f
     typedef double out_t;
-    ZigCtx z;
-    GammaPrm g;
-    template <class S> RS_DEV double sample(S &s, Tally &t) const { return gamma_sample(s, z, g, t); }
-};
-struct DistBeta {  // x = gamma(a,1) then y = gamma(b,1); x/(x+y) (continuous.py:215-218)
-    typedef double out_t;
+    static constexpr bool HALF = false;
     ZigCtx z;
     GammaPrm ga, gb;
+    double nu1, nu2;
+    int kind;
+    // beta / f / t samples are (first, second) pairs of sub-samples
+    RS_DEV bool paired() const { return kind != GK_GAMMA; }
+    template <class S> RS_DEV void skip_second(S &s, Tally &t) const {
+        if (kind == GK_T) gamma_sample(s, z, ga, t);
+        else gamma_sample(s, z, gb, t);
+    }
     template <class S> RS_DEV double sample(S &s, Tally &t) const {
+        if (kind == GK_T) {
+            double zn = std_norm(s, z, t);
+            double v = gamma_sample(s, z, ga, t);
+            return zn / sqrt(v / nu1);
+        }
         double x = gamma_sample(s, z, ga, t);
+        if (kind == GK_GAMMA) return x;
         double y = gamma_sample(s, z, gb, t);
-        return x / (x + y);
+        return kind == GK_BETA ? x / (x + y) : (x / nu1) / (y / nu2);
     }
 };
-struct DistLemire {  // bounded_uint(rng, b, 64), discrete.py:20-39: redraw while low < (2^64-b) % b
+struct DistLemire {  // bounded_uint(rng, b, 64) discrete.py:20-39 (+ m: bounded_int long_long, :42-55)
     typedef u64 out_t;
-    u64 b, thr;
+    static constexpr bool HALF = false;
+    u64 b, thr, m;
+    RS_DEV bool paired() const { return false; }
+    template <class S> RS_DEV void skip_second(S &, Tally &) const {}
     template <class S> RS_DEV u64 sample(S &s, Tally &) const {
         while (true) {
             u64 w = s.next();
-            if (w * b >= thr) return __umul64hi(w, b);
+            if (w * b >= thr) return m + __umul64hi(w, b);
         }
     }
     // word-level form: every lane consumes one word per step (no divergent redraw loops)
     RS_DEV bool accept(u64 w, u64 &o) const {
-        o = __umul64hi(w, b);
+        o = m + __umul64hi(w, b);
         return w * b >= thr;
+    }
+};
+enum { FK_NORMF = 0, FK_EXPF = 1 };
+struct DistF32 {  // normf / expf, continuous.py:136-154 (32-bit halves, f32 tables)
+    typedef float out_t;
+    static constexpr bool HALF = true;
+    ZigCtxF z;
+    double a, b;  // NORMF: mu, sd | EXPF: beta
+    int kind;
+    RS_DEV bool paired() const { return false; }
+    template <class S> RS_DEV void skip_second(S &, Tally &) const {}
+    template <class S> RS_DEV float sample(S &s, Tally &) const {
+        if (kind == FK_NORMF) return __double2float_rn(a + b * std_norm_f(s, z));
+        return __double2float_rn(a * std_exp_f(s, z));
+    }
+};
+struct DistU32 {  // bounded_uint(rng, b, 8|16|32) on halves (+ m: bounded_int int), discrete.py:14-55
+    typedef u32 out_t;
+    static constexpr bool HALF = true;
+    u64 b, thr, mask;
+    u32 m;
+    int width;
+    RS_DEV bool paired() const { return false; }
+    template <class S> RS_DEV void skip_second(S &, Tally &) const {}
+    template <class S> RS_DEV u32 sample(S &s, Tally &) const {
+        while (true) {
+            u32 o;
+            if (accept(s.next32(), o)) return o;
+        }
+    }
+    RS_DEV bool accept(u32 h, u32 &o) const {
+        u64 x = (u64)h & mask;
+        u64 mm = x * b;
+        o = m + (u32)(mm >> width);
+        return (mm & mask) >= thr;
     }
 };
 
@@ -644,6 +777,14 @@ struct VecWriter8 {
         if (first <= 1 && slot > 1) p[1] = v1;
         if (first <= 2 && slot > 2) p[2] = v2;
     }
+};
+
+template <class T>
+struct ScalarWriter {
+    T *ptr;
+    RS_DEV void init(T *out, u64 start) { ptr = out + start; }
+    RS_DEV void put(T v) { *ptr++ = v; }
+    RS_DEV void finish() {}
 };
 
 template <class T>

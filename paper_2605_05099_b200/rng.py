@@ -41,16 +41,30 @@ _STREAM_METHODS = {  # rng.py:27-35
 SCALAR_NAMES = ("u01", "u01f", "unif", "uniff", "norm", "normf", "exp", "expf", "lognormal", "gamma", "beta",
                 "chi2", "t", "f", "gumbel", "pareto", "gpd", "weibull", "skew_normal")
 DISCRETE_NAMES = ("uint8", "uint16", "uint32", "uint64", "int", "long_long")
-DEVICE_DISTS = ("u01", "u01f", "norm", "exp", "gamma", "beta", "uint64")
+_TRANSFORMED = ("lognormal", "gumbel", "pareto", "weibull", "gpd")  # continuous.py:361
+_WIDTH = {"uint8": 8, "uint16": 16, "uint32": 32, "uint64": 64}
 
-# accepted keyword parameters of each device sampler: (allowed, required) -- continuous.py signatures
+# keyword signatures of the reference samplers: (allowed, required) -- continuous.py:136-290
 _SIGNATURES = {
     "u01": ((), ()),
     "u01f": ((), ()),
+    "unif": (("a", "b"), ()),
+    "uniff": (("a", "b"), ()),
     "norm": (("mu", "var"), ()),
+    "normf": (("mu", "var"), ()),
     "exp": (("beta",), ()),
+    "expf": (("beta",), ()),
+    "lognormal": (("mu", "var"), ()),
     "gamma": (("alpha", "theta"), ("alpha",)),
     "beta": (("a", "b"), ("a", "b")),
+    "chi2": (("nu",), ("nu",)),
+    "t": (("nu",), ("nu",)),
+    "f": (("nu1", "nu2"), ("nu1", "nu2")),
+    "gumbel": (("mu", "beta"), ()),
+    "pareto": (("alpha", "xm"), ("alpha",)),
+    "gpd": (("xi", "mu", "sigma"), ("xi",)),
+    "weibull": (("k", "lam"), ("k",)),
+    "skew_normal": (("alpha", "mu", "sigma"), ()),
 }
 _TALLY_NAMES = ("norm", "exp", "gamma")
 
@@ -78,8 +92,14 @@ def _cuda_stream_ptr(device):
 def _out_dtype(dist):
     if dist == "uint64":
         return torch.uint64
-    if dist == "u01f":
+    if dist in ("u01f", "uniff", "normf", "expf"):
         return torch.float32
+    if dist in ("uint8", "uint16", "uint32"):
+        return torch.uint32
+    if dist == "int":
+        return torch.int32
+    if dist == "long_long":
+        return torch.int64
     return torch.float64
 
 
@@ -296,60 +316,82 @@ class Rng:
     def fill(self, dist, params=None, n=1, out=None):
         """n draws of a named distribution on the GPU (rng.py:223-241).
 
-        Returns a 1-D device tensor (uint64 / float64 / float32 for u01f);
-        `.tolist()` gives the reference's list. `out` may be a device tensor or a
-        host numpy array (staged through device memory by the library)."""
+        Returns a 1-D device tensor (uint64 / float64; float32 for the 32-bit-half
+        laws u01f/uniff/normf/expf; uint32 for uint8/16/32; int32 / int64 for
+        int / long_long); `.tolist()` gives the reference's list. `out` may be a
+        device tensor or a host numpy array (staged through device memory)."""
         params = dict(params or {})
         if dist in ("perm", "sample"):
             raise NotImplementedError("%s draws are sequences, not bulk fills; not on the B200 fill path" % dist)
-        if dist in SCALAR_NAMES:
-            n = int(n)
-            if n < 0:
-                raise ValueError("draw count must be >= 0")
-            if dist not in DEVICE_DISTS:
-                raise NotImplementedError("distribution %r is not on the B200 fill path yet" % dist)
-            fp = self._continuous_params(dist, params, n)
-            return self.device_fill(dist, fp, [], n, out)
         n = int(n)
         if n < 0:
             raise ValueError("draw count must be >= 0")
+        if dist in SCALAR_NAMES:
+            fp = self._continuous_params(dist, params, n)
+            return self.device_fill(dist, fp, [], n, out)
         if dist in DISCRETE_NAMES:
-            if dist != "uint64":
-                raise NotImplementedError("distribution %r is not on the B200 fill path yet" % dist)
-            b = int(params.get("b", 0))
-            if n > 0 and (b < 0 or b > (1 << 64)):
-                raise ValueError("bound must be in [0, 2^64]")
-            ip = [0, 1] if b == 1 << 64 else [b, 0]
-            return self.device_fill("uint64", [], ip, n, out)
+            ip = self._discrete_params(dist, params, n)
+            return self.device_fill(dist, [], ip, n, out)
         raise ValueError("unknown discrete distribution %r" % dist)
 
+    def _discrete_params(self, dist, params, n):
+        """discrete.py:103-118 + bounded_uint/bounded_int checks (per call, so n >= 1 only)."""
+        if dist in _WIDTH:
+            width = _WIDTH[dist]
+            b = int(params.get("b", 0))
+            if n > 0 and (b < 0 or b > (1 << width)):
+                raise ValueError("bound must be in [0, 2^%d]" % width)
+            if width == 64:
+                return [0, 1, 0, 0] if b == 1 << 64 else [b, 0, 0, 0]
+            return [b, width, 0, 0]
+        width = 32 if dist == "int" else 64
+        half = 1 << (width - 1)
+        m, hi = int(params.get("m", -half)), int(params.get("n", half - 1))
+        if n > 0 and not (-half <= m <= hi <= half - 1):
+            raise ValueError("range [%d, %d] does not fit a signed %d-bit span" % (m, hi, width))
+        span = hi - m + 1
+        full = 1 if span == 1 << width else 0
+        return [0 if full else span, width, m & MASK64, full]
+
     def _continuous_params(self, dist, params, n):
-        """Reference validation order (continuous.py:413-431 + sampler bodies):
-        nothing is checked for n == 0; otherwise bad keywords -> 'bad parameters',
-        then the sampler's own value checks, before any word is consumed."""
+        """Reference validation order (continuous.py:413-431 + sampler bodies): the
+        numpy-vectorised transform path (default mode) validates its parameters even
+        for n == 0 (continuous.py:364-410); every other sampler validates per call, i.e.
+        nothing for n == 0, then bad keywords -> 'bad parameters', then its own value
+        checks -- always before any word is consumed."""
+        vec = dist in _TRANSFORMED and not self.bitexact
+        if vec:
+            return self._vectorized_params(dist, params)
         if n == 0:
-            return [0.0, 0.0]
+            return [0.0] * 4
         allowed, required = _SIGNATURES[dist]
         if any(k not in allowed for k in params) or any(k not in params for k in required):
             raise ValueError("bad parameters for %s: %r" % (dist, sorted(params)))
-        if dist == "norm":
-            mu = float(params.get("mu", 0.0))
-            var = float(params.get("var", 1.0))
-            if not var >= 0.0:
-                raise ValueError("normal variance must be >= 0")
-            return [mu, var]
-        if dist == "exp":
-            beta = float(params.get("beta", 1.0))
+        g = params.get
+        if dist in ("u01", "u01f"):
+            return [0.0] * 4
+        if dist in ("unif", "uniff"):
+            a, b = float(g("a", 0.0)), float(g("b", 1.0))
+            if not b > a:
+                raise ValueError("%s needs b > a" % dist)
+            return [a, b, 0.0, 0.0]
+        if dist in ("norm", "normf", "lognormal"):
+            mu, var = float(g("mu", 0.0)), float(g("var", 1.0))
+            if not var >= 0.0:  # lognormal = det_exp(norm(...)) checks as "normal"
+                raise ValueError("%s variance must be >= 0" % ("normf" if dist == "normf" else "normal"))
+            return [mu, var, 0.0, 0.0]
+        if dist in ("exp", "expf"):
+            beta = float(g("beta", 1.0))
             if not beta > 0.0:
-                raise ValueError("exponential scale must be > 0")
-            return [beta]
+                raise ValueError("exponential scale must be > 0" if dist == "exp" else "expf scale must be > 0")
+            return [beta, 0.0, 0.0, 0.0]
         if dist == "gamma":
-            alpha, theta = float(params["alpha"]), float(params.get("theta", 1.0))
+            alpha, theta = float(params["alpha"]), float(g("theta", 1.0))
             if not alpha > 0.0:
                 raise ValueError("gamma shape must be > 0")
             if not theta > 0.0:
                 raise ValueError("gamma scale must be > 0")
-            return [alpha, theta]
+            return [alpha, theta, 0.0, 0.0]
         if dist == "beta":
             a, b = float(params["a"]), float(params["b"])
             if not a > 0.0:
@@ -359,8 +401,53 @@ class Rng:
                 # consume exactly that one gamma(a) sample, then fail.
                 self.device_fill("gamma", [a, 1.0], [], 1)
                 raise ValueError("gamma shape must be > 0")
-            return [a, b]
-        return []
+            return [a, b, 0.0, 0.0]
+        if dist in ("chi2", "t"):
+            nu = float(params["nu"])
+            if not nu > 0.0:
+                raise ValueError("%s degrees of freedom must be > 0" % dist)
+            return [nu, 0.0, 0.0, 0.0]
+        if dist == "f":
+            nu1, nu2 = float(params["nu1"]), float(params["nu2"])
+            if not (nu1 > 0.0 and nu2 > 0.0):
+                raise ValueError("f degrees of freedom must be > 0")
+            return [nu1, nu2, 0.0, 0.0]
+        if dist == "skew_normal":
+            alpha, mu, sigma = float(g("alpha", 0.0)), float(g("mu", 0.0)), float(g("sigma", 1.0))
+            if not sigma > 0.0:
+                raise ValueError("skew_normal scale must be > 0")
+            return [alpha, mu, sigma, 0.0]
+        return self._vectorized_params(dist, params)  # bitexact transforms: same checks
+
+    @staticmethod
+    def _vectorized_params(dist, params):
+        """_fill_vectorized's parameter reading (continuous.py:364-410): unknown keys are
+        ignored, a missing required key raises KeyError, checks run even for n == 0."""
+        g = params.get
+        if dist == "lognormal":
+            mu, var = float(g("mu", 0.0)), float(g("var", 1.0))
+            if not var >= 0.0:
+                raise ValueError("lognormal variance must be >= 0")
+            return [mu, var, 0.0, 0.0]
+        if dist == "gumbel":
+            mu, b = float(g("mu", 0.0)), float(g("beta", 1.0))
+            if not b > 0.0:
+                raise ValueError("gumbel scale must be > 0")
+            return [mu, b, 0.0, 0.0]
+        if dist == "pareto":
+            alpha, xm = float(params["alpha"]), float(g("xm", 1.0))
+            if not (alpha > 0.0 and xm > 0.0):
+                raise ValueError("pareto needs alpha > 0 and xm > 0")
+            return [alpha, xm, 0.0, 0.0]
+        if dist == "weibull":
+            k, lam = float(params["k"]), float(g("lam", 1.0))
+            if not (k > 0.0 and lam > 0.0):
+                raise ValueError("weibull needs k > 0 and lambda > 0")
+            return [k, lam, 0.0, 0.0]
+        xi, mu, sigma = float(params["xi"]), float(g("mu", 0.0)), float(g("sigma", 1.0))  # gpd
+        if not sigma > 0.0:
+            raise ValueError("gpd scale must be > 0")
+        return [xi, mu, sigma, 0.0]
 
     # ---------------------------------------------------------------- scalar conveniences
     @_op
@@ -444,13 +531,11 @@ def fill_streams(engine, seed, spawn_prefix, j0, n_streams, dist, params, n_per_
     eid = engines.normalize(engine)
     params = dict(params or {})
     n_streams, n_per_stream = int(n_streams), int(n_per_stream)
-    if dist == "uint64":
-        b = int(params.get("b", 0))
-        fp, ip = [0.0] * 4, ([0, 1] if b == 1 << 64 else [b, 0])
+    probe = Rng(engines.make(eid))
+    if dist in DISCRETE_NAMES:
+        fp, ip = [0.0] * 4, probe._discrete_params(dist, params, 1)
     else:
-        probe = Rng(engines.make(eid))
-        fp = probe._continuous_params(dist, params, 1) + [0.0] * 2
-        ip = [0, 0]
+        fp, ip = probe._continuous_params(dist, params, 1), [0, 0, 0, 0]
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     out = torch.empty((n_streams, n_per_stream), dtype=_out_dtype(dist), device=dev)
     seedw = [int(w) & MASK64 for w in seed]

@@ -45,9 +45,15 @@ def f64bits(vals):
 
 
 def out_array(dist, vals):
-    if dist.startswith("uint"):
+    if dist == "uint64":
         return np.asarray(vals, dtype=np.uint64)
-    if dist in ("u01f",):
+    if dist in ("uint8", "uint16", "uint32"):
+        return np.asarray(vals, dtype=np.uint32)
+    if dist == "int":
+        return np.asarray(vals, dtype=np.int32)
+    if dist == "long_long":
+        return np.asarray(vals, dtype=np.int64)
+    if dist in ("u01f", "uniff", "normf", "expf"):
         return np.asarray(vals, dtype=np.float32)
     return np.asarray(vals, dtype=np.float64)
 
@@ -66,11 +72,11 @@ def buf_sha(words):
 CASES = []
 
 
-def case(name, engine, seed, dist, params, n, spawn=(), fm=False, pre=(), keep=None):
+def case(name, engine, seed, dist, params, n, spawn=(), fm=False, pre=(), keep=None, bitexact=False):
     if keep is None:
         keep = n <= 20000
     CASES.append(dict(name=name, engine=engine, seed=list(seed), spawn=list(spawn), full_mantissa=fm,
-                      pre=[list(p) for p in pre], dist=dist, params=params, n=n, keep=keep))
+                      pre=[list(p) for p in pre], dist=dist, params=params, n=n, keep=keep, bitexact=bitexact))
 
 
 # BASELINE configs (prefix sizes the reference finishes in seconds)
@@ -119,6 +125,26 @@ for e in ENG:
         case("edge_%s_bounded_%d" % (tag, b), e, [15], "uint64", {"b": b}, 400)
     case("edge_%s_stdnorm_tail" % tag, e, [16], "norm", {}, 40000, keep=False)
     case("edge_%s_exp_tail" % tag, e, [17], "exp", {}, 40000, keep=False)
+# derived laws, transforms and narrower / signed integers
+DERIVED = [("unif", {"a": -2.0, "b": 3.0}), ("unif", {}), ("uniff", {"a": -2.0, "b": 3.0}),
+           ("normf", {"mu": 1.0, "var": 4.0}), ("normf", {}), ("expf", {"beta": 2.5}), ("expf", {}),
+           ("lognormal", {"mu": 0.5, "var": 0.25}), ("chi2", {"nu": 3.0}), ("chi2", {"nu": 0.8}),
+           ("t", {"nu": 5.0}), ("f", {"nu1": 3.0, "nu2": 7.0}), ("gumbel", {"mu": 1.0, "beta": 2.0}),
+           ("pareto", {"alpha": 2.5}), ("gpd", {"xi": 0.3}), ("gpd", {"xi": -0.2, "sigma": 2.0}),
+           ("gpd", {"xi": 0.0, "mu": 1.0}), ("weibull", {"k": 1.7}), ("skew_normal", {"alpha": 3.0, "mu": 1.0, "sigma": 2.0}),
+           ("skew_normal", {}), ("uint8", {"b": 200}), ("uint8", {}), ("uint16", {"b": 1000}), ("uint16", {"b": 1024}),
+           ("uint32", {"b": 3000000001}), ("uint32", {}), ("uint32", {"b": 1 << 32}), ("int", {"m": -5, "n": 17}),
+           ("int", {}), ("int", {"m": -(1 << 31), "n": 0}), ("long_long", {"m": -10 ** 15, "n": 10 ** 18}),
+           ("long_long", {}), ("long_long", {"m": 7, "n": 7 + (1 << 40) - 1})]
+TRANSFORMED = ("lognormal", "gumbel", "pareto", "weibull", "gpd")
+for e in ("x256**", "pcg64", "philox", "sfc64", "ranlux++"):
+    tag = e.replace("+", "p").replace("*", "s")
+    for i, (dist, params) in enumerate(DERIVED):
+        case("derived_%s_%s_%d" % (tag, dist, i), e, [100 + i], dist, params, 1500, pre=[("u32", 1)],
+             fm=(i % 2 == 1), bitexact=True)
+        if dist in TRANSFORMED:
+            case("derived_%s_%s_%d_vec" % (tag, dist, i), e, [100 + i], dist, params, 1500, pre=[("u32", 1)])
+
 # long runs for the diagnostic tallies (gate 04 reads them)
 case("tally_sfc64_norm", "sfc64", [40401], "norm", {}, 1 << 18, keep=False)
 case("tally_sfc64_exp", "sfc64", [40402], "exp", {}, 1 << 18, keep=False)
@@ -137,6 +163,7 @@ def run_pre(rng, pre):
 def run_case(c):
     rng = state_io.create(c["engine"], seed=c["seed"], spawn_key=tuple(c["spawn"]))
     rng.set_full_mantissa(c["full_mantissa"])
+    rng.set_bitexact(c.get("bitexact", False))
     start_state = rng.get_state()
     run_pre(rng, c["pre"])
     vals = rng.fill(c["dist"], dict(c["params"]), c["n"])
