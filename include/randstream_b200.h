@@ -105,7 +105,7 @@ typedef struct rs_stream {
     int32_t bitexact;       /* Rng.bitexact (only affects transform families) */
     int32_t has_pending;    /* WordBuffer.pending is not None */
     uint64_t pending;       /* the buffered high half (u32) */
-    uint64_t state[9];      /* engine.get_state() words */
+    uint64_t state[32];     /* engine.get_state() words (32 for the interleaved engines) */
     uint64_t buf[RS_BUFFER_CAPACITY];
     int32_t fill;           /* len(WordBuffer.words): 0 or 144 */
     int32_t cursor;         /* WordBuffer.cursor */

@@ -34,7 +34,8 @@ typedef unsigned __int128 u128;
 #define M64 0xFFFFFFFFFFFFFFFFULL
 
 /* engine ids follow the reference registry order, src/engines/__init__.py:11-26 */
-enum { E_X256PP = 1, E_X256SS = 2, E_PCG64 = 5, E_PHILOX = 6, E_SFC64 = 8, E_RANLUX = 10 };
+enum { E_X256PP = 1, E_X256SS = 2, E_PCG64 = 5, E_PHILOX = 6, E_SFC64 = 8, E_RANLUX = 10,
+       E_X256PP_SIMD = 12, E_X256SS_SIMD = 13, E_SFC64_SIMD = 14 };
 
 /* distribution ids, shared with include/randstream_b200.h */
 enum { D_UINT64 = 1, D_U01 = 2, D_U01F = 3, D_NORM = 4, D_EXP = 5, D_GAMMA = 6, D_BETA = 7,
@@ -45,7 +46,7 @@ enum { D_UINT64 = 1, D_U01 = 2, D_U01F = 3, D_NORM = 4, D_EXP = 5, D_GAMMA = 6, 
 typedef struct orc_rng {
     int eid;
     int full_mantissa;
-    uint64_t st[9];            /* engine state, get_state() order */
+    uint64_t st[32];           /* engine state, get_state() order (32 words for the 8-lane engines) */
     uint64_t buf[CAP];
     int fill, cursor;
     int has_pending;
@@ -232,16 +233,32 @@ static void gen_ranlux(uint64_t *s, uint64_t *out, int n) {
     }
 }
 
-static int engine_chunk(int eid) { return eid == E_PHILOX ? 4 : eid == E_RANLUX ? 9 : 1; }
 static int engine_state_words(int eid) {
-    switch (eid) { case E_PHILOX: return 6; case E_RANLUX: return 9; default: return 4; }
+    switch (eid) {
+    case E_PHILOX: return 6;
+    case E_RANLUX: return 9;
+    case E_X256PP_SIMD: case E_X256SS_SIMD: case E_SFC64_SIMD: return 32;
+    default: return 4;
+    }
 }
 static int engine_seed_words(int eid) {
-    switch (eid) { case E_PHILOX: return 2; case E_SFC64: return 3; case E_RANLUX: return 9; default: return 4; }
+    switch (eid) { case E_PHILOX: return 2; case E_SFC64: case E_SFC64_SIMD: return 3; case E_RANLUX: return 9; default: return 4; }
+}
+
+/* 8-lane interleaved engines, src/engines/interleave.py:71-76: word i from lane i mod 8 */
+static void gen_simd(int base, uint64_t *s, uint64_t *out, int n) {
+    for (int i = 0; i < n; i++) {
+        uint64_t *l = s + 4 * (i & 7);
+        if (base == E_SFC64) gen_sfc(l, out + i, 1);
+        else gen_x256(l, out + i, 1, base == E_X256SS);
+    }
 }
 
 static void engine_generate(int eid, uint64_t *s, uint64_t *out, int n) {
     switch (eid) {
+    case E_X256PP_SIMD: gen_simd(E_X256PP, s, out, n); break;
+    case E_X256SS_SIMD: gen_simd(E_X256SS, s, out, n); break;
+    case E_SFC64_SIMD: gen_simd(E_SFC64, s, out, n); break;
     case E_X256PP: gen_x256(s, out, n, 0); break;
     case E_X256SS: gen_x256(s, out, n, 1); break;
     case E_PCG64: gen_pcg(s, out, n); break;
@@ -291,10 +308,31 @@ void orc_seed_words(const uint64_t *ent, int nent, const uint64_t *spawn, int ns
     }
 }
 
+void orc_x256_charpoly(uint64_t *out5);
+void orc_x_pow2k_mod(int k, const uint64_t *c5, uint64_t *out5);
+void orc_x256_apply_poly(uint64_t *s, const uint64_t *poly5);
+
 /* seed_from for each engine: xorfam.py:66-70, pcg.py:81-84, counter.py:139-141,
- * sfc.py:53-55, ranlux.py:106-110 */
+ * sfc.py:53-55, ranlux.py:106-110, interleave.py:127-130,212-215 */
 static void engine_seed_from(int eid, uint64_t *s, const uint64_t *w) {
     switch (eid) {
+    case E_X256PP_SIMD: case E_X256SS_SIMD: {
+        uint64_t base[4];
+        memcpy(base, w, 32);
+        if (!(base[0] | base[1] | base[2] | base[3])) base[0] = 1;
+        uint64_t p[5], poly[5];
+        orc_x256_charpoly(p);
+        orc_x_pow2k_mod(253, p, poly);   /* lanes 2^253 steps apart (interleave.py:201-208) */
+        memcpy(s, base, 32);
+        for (int k = 1; k < 8; k++) { memcpy(s + 4 * k, s + 4 * (k - 1), 32); orc_x256_apply_poly(s + 4 * k, poly); }
+        break;
+    }
+    case E_SFC64_SIMD:
+        for (int k = 0; k < 8; k++) {
+            s[4 * k] = w[0]; s[4 * k + 1] = w[1]; s[4 * k + 2] = w[2];
+            s[4 * k + 3] = 1 + (uint64_t)k * (1ULL << 61);
+        }
+        break;
     case E_X256PP: case E_X256SS:
         memcpy(s, w, 32);
         if (!(s[0] | s[1] | s[2] | s[3])) s[0] = 1;

@@ -22,8 +22,9 @@ import numpy as np
 HERE = pathlib.Path(__file__).resolve().parent
 LIB_PATH = HERE / "liboracle.so"
 
-ENGINE_IDS = {"x256++": 1, "x256**": 2, "pcg64": 5, "philox": 6, "sfc64": 8, "ranlux++": 10}
-STATE_WORDS = {1: 4, 2: 4, 5: 4, 6: 6, 8: 4, 10: 9}
+ENGINE_IDS = {"x256++": 1, "x256**": 2, "pcg64": 5, "philox": 6, "sfc64": 8, "ranlux++": 10,
+              "x256++simd": 12, "x256**simd": 13, "sfc64simd": 14}
+STATE_WORDS = {1: 4, 2: 4, 5: 4, 6: 6, 8: 4, 10: 9, 12: 32, 13: 32, 14: 32}
 DIST_IDS = {"uint64": 1, "u01": 2, "u01f": 3, "norm": 4, "exp": 5, "gamma": 6, "beta": 7, "stdnorm": 8,
             "unif": 9, "uniff": 10, "normf": 11, "expf": 12, "lognormal": 13, "chi2": 14, "t": 15, "f": 16,
             "gumbel": 17, "pareto": 18, "gpd": 19, "weibull": 20, "skew_normal": 21,
@@ -39,7 +40,7 @@ class _Rng(ctypes.Structure):
     _fields_ = [
         ("eid", ctypes.c_int),
         ("full_mantissa", ctypes.c_int),
-        ("st", ctypes.c_uint64 * 9),
+        ("st", ctypes.c_uint64 * 32),
         ("buf", ctypes.c_uint64 * CAP),
         ("fill", ctypes.c_int),
         ("cursor", ctypes.c_int),
@@ -288,7 +289,7 @@ def ranlux_jump(state, k):
 
 def engine_generate(engine, state, n):
     eid = ENGINE_IDS[engine]
-    s, _ = _u64arr(list(state) + [0] * (9 - len(state)))
+    s, _ = _u64arr(list(state) + [0] * (32 - len(state)))
     out = (ctypes.c_uint64 * n)()
     lib().orc_engine_generate(eid, s, out, n)
     return [int(v) for v in out], [int(s[i]) for i in range(STATE_WORDS[eid])]

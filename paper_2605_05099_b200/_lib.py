@@ -31,7 +31,7 @@ class RsStream(ctypes.Structure):
         ("bitexact", ctypes.c_int32),
         ("has_pending", ctypes.c_int32),
         ("pending", ctypes.c_uint64),
-        ("state", ctypes.c_uint64 * 9),
+        ("state", ctypes.c_uint64 * 32),
         ("buf", ctypes.c_uint64 * CAP),
         ("fill", ctypes.c_int32),
         ("cursor", ctypes.c_int32),

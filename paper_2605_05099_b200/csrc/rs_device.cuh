@@ -175,6 +175,27 @@ struct EngSfc {  // sfc.py:25-36
     }
 };
 
+// sfc64simd (interleave.py:172-187): 8 sfc64 lanes, word i from lane i mod 8
+struct EngSfcSimd {
+    EngSfc l[8];
+    int k;
+    RS_DEV u64 next() {
+        u64 r;
+        switch (k) {  // constant-indexed registers (no local-memory array)
+        case 0: r = l[0].next(); break;
+        case 1: r = l[1].next(); break;
+        case 2: r = l[2].next(); break;
+        case 3: r = l[3].next(); break;
+        case 4: r = l[4].next(); break;
+        case 5: r = l[5].next(); break;
+        case 6: r = l[6].next(); break;
+        default: r = l[7].next(); break;
+        }
+        k = (k + 1) & 7;
+        return r;
+    }
+};
+
 // ranlux++: x <- x*A mod m, m = 2^576 - 2^240 + 1 (ranlux.py:36-61); any exact
 // reduction yields the same canonical residue.
 RS_DEV void rlx_mulmod_dev(const u64 *x, const u64 *y, u64 *out) {

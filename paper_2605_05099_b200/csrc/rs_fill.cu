@@ -61,6 +61,8 @@ struct FillPlan {
     u64 pcg_m[MAXLEV][2], pcg_a[MAXLEV][2];
     u64 rlx[MAXLEV][9];
     u64 rk0[10], rk1[10];         // philox round keys (counter.py:95-96)
+    u64 lanes[32];                // interleaved engines: the 8 lane states (lane-major)
+    u64 G, Gpad;                  // interleaved fixed fills: step groups (real / padded)
     int vec_ok;                   // counter-based fill: outputs 32-byte aligned per block
     double fp[4];
     u64 ip[4];
@@ -88,7 +90,7 @@ struct DevResult {
     u32 flag;        // entry resolution not at a fixed point
     u32 pad;
     u64 tally[6];
-    u64 serial_state[9];
+    u64 serial_state[32];
     u64 serial_buf[CAP];
     u64 serial_consumed;
 };
@@ -111,6 +113,7 @@ template <> struct EngOf<RS_ENG_PCG64> { typedef EngPcg type; };
 template <> struct EngOf<RS_ENG_PHILOX> { typedef EngPhilox type; };
 template <> struct EngOf<RS_ENG_RANLUX> { typedef EngRanlux type; };
 template <> struct EngOf<RS_ENG_SFC64> { typedef EngSfc type; };
+template <> struct EngOf<RS_ENG_SFC64_SIMD> { typedef EngSfcSimd type; };
 
 // Parse source for engines whose words are expensive (Philox-4x64, ranlux++): the
 // chunk's engine words are materialized once by the coalesced fixed-fill kernel and
@@ -150,6 +153,13 @@ __device__ __forceinline__ void make_engine(const FillPlan &p, u32 t, typename E
         e.A = p.rlx_A;
     } else if constexpr (E == RS_ENG_SFC64) {
         e.a = p.base[0]; e.b = p.base[1]; e.c = p.base[2]; e.w = p.base[3];
+    } else if constexpr (E == RS_ENG_SFC64_SIMD) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            e.l[k].a = p.lanes[4 * k]; e.l[k].b = p.lanes[4 * k + 1];
+            e.l[k].c = p.lanes[4 * k + 2]; e.l[k].w = p.lanes[4 * k + 3];
+        }
+        e.k = 0;
     } else if constexpr (E == RS_ENG_MEM) {
         e.w = p.words;
         e.idx = (u64)t * p.L;
@@ -325,7 +335,10 @@ __global__ void __launch_bounds__(BLOCK) k_x256_setup(const __grid_constant__ Fi
                                                       u64 *states) {
     const u32 lane = threadIdx.x & 31;
     const u64 w = ((u64)blockIdx.x * BLOCK + threadIdx.x) >> 5;
-    u64 v[4] = {p.base[0], p.base[1], p.base[2], p.base[3]};
+    // gridDim.y == 8: interleaved engine, one grid row per lane (base = that lane's state)
+    const u64 *b0 = gridDim.y > 1 ? p.lanes + 4 * blockIdx.y : p.base;
+    states += (u64)blockIdx.y * 4 * ((u64)gridDim.x * BLOCK);
+    u64 v[4] = {b0[0], b0[1], b0[2], b0[3]};
     u64 ww = w;
     for (int k = 0; ww; k++, ww >>= 1)
         if (ww & 1) warp_matvec(ML + (u64)(1 + k) * 1024, v, v);
@@ -724,13 +737,57 @@ __global__ void __launch_bounds__(BLOCK) k_philox_fixed(const __grid_constant__ 
     }
 }
 
+// Interleaved xoshiro engines (interleave.py:94-166): word j of the stream is lane
+// j mod 8 at step j / 8. Thread t = 8 g + k runs lane k over steps
+// [g Ls, (g+1) Ls) from its own GF(2)-jumped state, so the 8 threads of a group emit
+// 8 consecutive words per step (64 contiguous bytes per group and step).
+template <int E, int MODE>
+__global__ void __launch_bounds__(BLOCK) k_simd_fixed(const __grid_constant__ FillPlan p) {
+    const u64 t = (u64)blockIdx.x * BLOCK + threadIdx.x;
+    const u64 g = t >> 3, k = t & 7;
+    if (t == 0) {  // the buffered prefix and a pending half
+        if constexpr (is_half(MODE)) {
+            u32 *out = (u32 *)p.out;
+            if (p.pending_used) out[0] = (u32)fx_map<MODE>(p, p.pending_val);
+            for (int i = 0; i < p.P; i++) {
+                u64 f = (u64)p.pending_used + 2ULL * i;
+                u64 q = fx_map<MODE>(p, p.prefix[i]);
+                if (f < p.n) out[f] = (u32)q;
+                if (f + 1 < p.n) out[f + 1] = (u32)(q >> 32);
+            }
+        } else {
+            u64 *out = (u64 *)p.out;
+            for (int i = 0; i < p.P && (u64)i < p.n; i++) out[i] = fx_map<MODE>(p, p.prefix[i]);
+        }
+    }
+    if (g >= p.G) return;
+    EngX256<E == RS_ENG_X256SS_SIMD> e;
+    e.load(p.x256_states + 4 * (k * p.Gpad + g));
+    const u64 steps = (p.weng + 7) / 8;
+    u64 s0 = g * p.L, s1 = s0 + p.L < steps ? s0 + p.L : steps;
+    for (u64 st = s0; st < s1; st++) {
+        u64 q = fx_map<MODE>(p, e.next());
+        u64 j = 8 * st + k;
+        if (j >= p.weng) break;
+        if constexpr (is_half(MODE)) {
+            u32 *out = (u32 *)p.out;
+            u64 f = (u64)p.pending_used + 2ULL * ((u64)p.P + j);
+            if (f < p.n) out[f] = (u32)q;
+            if (f + 1 < p.n) out[f + 1] = (u32)(q >> 32);
+        } else {
+            ((u64 *)p.out)[(u64)p.P + j] = q;
+        }
+    }
+}
+
 // ----------------------------------------------------------------------------- serial (sfc64 single stream)
 // sfc64 has no skip-ahead (rng.py:162-163): a single stream is parsed by one
 // thread; per-stream mode (k_streams) is the parallel path for sfc64. The
 // thread also rebuilds the reference's post-fill WordBuffer: it snapshots the
 // engine at every 144-word refill boundary and replays the last refill.
+template <class EN>
 struct SerialSrc {
-    EngSfc e, snap;
+    EN e, snap;
     const u64 *pre;
     int npre;
     u64 eng, pos;
@@ -743,8 +800,9 @@ struct SerialSrc {
     }
 };
 
+template <class EN>
 struct SerialHSrc {
-    SerialSrc *w;
+    SerialSrc<EN> *w;
     u64 pos;
     u32 hi, pv;
     bool have, pend;
@@ -772,13 +830,14 @@ __device__ u64 fx_map_rt(const FillPlan &p, u64 w) {
 
 // D < 0: fixed-consumption map p.fmode; otherwise a sampler family. end_pos is in the
 // family's stream units (halves for u32-fed samplers and half modes).
-template <int D>
+template <int D, int E>
 __global__ void k_serial(const __grid_constant__ FillPlan p, DevResult *res) {
     __shared__ ZigFast sm[256];
     stage_tables(p, sm);
     if (threadIdx.x != 0) return;
-    SerialSrc s;
-    make_engine<RS_ENG_SFC64>(p, 0, s.e);
+    typedef typename EngOf<E>::type EN;
+    SerialSrc<EN> s;
+    make_engine<E>(p, 0, s.e);
     s.snap = s.e;
     s.pre = p.prefix;
     s.npre = p.P;
@@ -807,7 +866,7 @@ __global__ void k_serial(const __grid_constant__ FillPlan p, DevResult *res) {
         typedef typename DistOf<D>::type::out_t T;
         T *out = (T *)p.out;
         if constexpr (DistOf<D>::type::HALF) {
-            SerialHSrc h{&s, 0, 0, p.pending_val, false, p.pending_used != 0};
+            SerialHSrc<EN> h{&s, 0, 0, p.pending_val, false, p.pending_used != 0};
             for (u64 i = 0; i < p.n; i++) out[i] = d.sample(h, tl);
             res->end_pos = h.pos;
         } else {
@@ -818,11 +877,18 @@ __global__ void k_serial(const __grid_constant__ FillPlan p, DevResult *res) {
     res->tally[0] = tl.norm_att; res->tally[1] = tl.norm_pdf; res->tally[2] = tl.exp_att;
     res->tally[3] = tl.exp_pdf; res->tally[4] = tl.gamma_att; res->tally[5] = 0;
     res->serial_consumed = s.eng;
-    EngSfc f = s.snap;
+    EN f = s.snap;
     if (s.eng > 0)
         for (int i = 0; i < CAP; i++) res->serial_buf[i] = f.next();
-    res->serial_state[0] = f.a; res->serial_state[1] = f.b;
-    res->serial_state[2] = f.c; res->serial_state[3] = f.w;
+    if constexpr (E == RS_ENG_SFC64_SIMD) {
+        for (int k = 0; k < 8; k++) {
+            res->serial_state[4 * k] = f.l[k].a; res->serial_state[4 * k + 1] = f.l[k].b;
+            res->serial_state[4 * k + 2] = f.l[k].c; res->serial_state[4 * k + 3] = f.l[k].w;
+        }
+    } else {
+        res->serial_state[0] = f.a; res->serial_state[1] = f.b;
+        res->serial_state[2] = f.c; res->serial_state[3] = f.w;
+    }
 }
 
 // ----------------------------------------------------------------------------- per-stream mode
@@ -1138,7 +1204,10 @@ VarKernels var_kernels_e(int fam) {
     default: return var_kernels_ed<E, FAM_LEMIRE>();
     }
 }
-bool parse_from_memory(int e) { return e == RS_ENG_PHILOX || e == RS_ENG_RANLUX; }
+bool parse_from_memory(int e) {
+    return e == RS_ENG_PHILOX || e == RS_ENG_RANLUX || e == RS_ENG_X256PP_SIMD || e == RS_ENG_X256SS_SIMD;
+}
+bool is_serial(int e) { return e == RS_ENG_SFC64 || e == RS_ENG_SFC64_SIMD; }
 VarKernels var_kernels(int e, int fam) {
     switch (e) {
     case RS_ENG_X256SS: return var_kernels_e<RS_ENG_X256SS>(fam);
@@ -1183,15 +1252,35 @@ const void *philox_kernel(int mode) {
     static int variant = getenv("RS_PHILOX_VARIANT") ? atoi(getenv("RS_PHILOX_VARIANT")) : 1;
     return variant == 0 ? philox_kernel_v<0>(mode) : philox_kernel_v<1>(mode);
 }
-const void *serial_kernel(int fam, int fixed_mode) {
-    if (fixed_mode >= 0) return (const void *)k_serial<-1>;
+template <int E>
+const void *serial_kernel_e(int fam, int fixed_mode) {
+    if (fixed_mode >= 0) return (const void *)k_serial<-1, E>;
     switch (fam) {
-    case FAM_NORM: return (const void *)k_serial<FAM_NORM>;
-    case FAM_EXP: return (const void *)k_serial<FAM_EXP>;
-    case FAM_GAMMA: return (const void *)k_serial<FAM_GAMMA>;
-    case FAM_F32: return (const void *)k_serial<FAM_F32>;
-    case FAM_U32: return (const void *)k_serial<FAM_U32>;
-    default: return (const void *)k_serial<FAM_LEMIRE>;
+    case FAM_NORM: return (const void *)k_serial<FAM_NORM, E>;
+    case FAM_EXP: return (const void *)k_serial<FAM_EXP, E>;
+    case FAM_GAMMA: return (const void *)k_serial<FAM_GAMMA, E>;
+    case FAM_F32: return (const void *)k_serial<FAM_F32, E>;
+    case FAM_U32: return (const void *)k_serial<FAM_U32, E>;
+    default: return (const void *)k_serial<FAM_LEMIRE, E>;
+    }
+}
+const void *serial_kernel(int engine, int fam, int fixed_mode) {
+    return engine == RS_ENG_SFC64_SIMD ? serial_kernel_e<RS_ENG_SFC64_SIMD>(fam, fixed_mode)
+                                       : serial_kernel_e<RS_ENG_SFC64>(fam, fixed_mode);
+}
+template <int MODE>
+const void *simd_kernel_m(int e) {
+    return e == RS_ENG_X256SS_SIMD ? (const void *)k_simd_fixed<RS_ENG_X256SS_SIMD, MODE>
+                                   : (const void *)k_simd_fixed<RS_ENG_X256PP_SIMD, MODE>;
+}
+const void *simd_kernel(int e, int mode) {
+    switch (mode) {
+    case FX_RAW: return simd_kernel_m<FX_RAW>(e);
+    case FX_U01: return simd_kernel_m<FX_U01>(e);
+    case FX_POW2: return simd_kernel_m<FX_POW2>(e);
+    case FX_WMAP: return simd_kernel_m<FX_WMAP>(e);
+    case FX_HMAP: return simd_kernel_m<FX_HMAP>(e);
+    default: return simd_kernel_m<FX_U01F>(e);
     }
 }
 
@@ -1469,12 +1558,12 @@ rs_status apply_consumption(rs_stream *s, u64 E, const DevResult *sr) {
     }
     u64 ep = E - P;
     u64 R = (ep + CAP - 1) / CAP;
-    if (s->engine == RS_ENG_SFC64) {  // rebuilt on the device by k_serial
+    if (is_serial(s->engine)) {  // rebuilt on the device by k_serial
         if (!sr || sr->serial_consumed != ep) {
             rs::set_error("serial fill bookkeeping mismatch");
             return RS_ERR_INTERNAL;
         }
-        memcpy(s->state, sr->serial_state, 32);
+        memcpy(s->state, sr->serial_state, 8 * rs::state_words(s->engine));
         memcpy(s->buf, sr->serial_buf, CAP * 8);
     } else {
         if (!rs::engine_advance_words(s->engine, s->state, (u128)(R - 1) * CAP)) {
@@ -1506,9 +1595,36 @@ rs_status get_out(DevCtx &c, void *out, size_t bytes, Staging &sg) {
     return RS_OK;
 }
 
+// interleaved xoshiro fixed fill: lane states jumped per step group on the device
+rs_status launch_simd(DevCtx &c, FillPlan &p, int mode, cudaStream_t st) {
+    const void *fn = simd_kernel(p.engine, mode);
+    u64 steps = (p.weng + 7) / 8;
+    if (steps == 0) steps = 1;
+    u64 Gfull = (u64)c.sms * occupancy(fn) * BLOCK / 8;  // one wave of lane-threads
+    u64 Ls = (steps + Gfull - 1) / Gfull;
+    if (Ls < 16) Ls = 16;
+    u64 G = (steps + Ls - 1) / Ls;
+    u64 Gpad = (G + BLOCK - 1) / BLOCK * BLOCK;
+    p.L = Ls;
+    p.G = G;
+    p.Gpad = Gpad;
+    rs_status rc = ensure_scratch(c, 8 * Gpad);
+    if (rc) return rc;
+    int lv = 0;
+    while ((1ULL << lv) < Gpad / 32) lv++;
+    u64 *ml;
+    if ((rc = x256_mats(c, Ls, lv, &ml))) return rc;
+    p.x256_states = c.states;
+    void *sargs[] = {&p, &ml, &c.states};
+    if ((rc = launch((const void *)k_x256_setup, dim3((unsigned)(Gpad / BLOCK), 8), dim3(BLOCK), sargs, st))) return rc;
+    void *args[] = {&p};
+    return launch(fn, dim3((unsigned)(8 * Gpad / BLOCK)), dim3(BLOCK), args, st);
+}
+
 // engine words [0, m.weng) of m.base into m.out (raw u64) with the fixed-fill kernels
 rs_status launch_raw_words(DevCtx &c, FillPlan &m, cudaStream_t st) {
     rs_status rc;
+    if (rs::simd_engine(m.engine)) return launch_simd(c, m, FX_RAW, st);
     if (m.engine == RS_ENG_PHILOX) {
         const void *fn = philox_kernel(FX_RAW);
         for (int i = 0; i < 10; i++) {
@@ -1547,16 +1663,18 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
     p.out = dout;
     p.out0 = 0;
     memcpy(p.base, s->state, sizeof p.base);
+    memcpy(p.lanes, s->state, sizeof p.lanes);
     const u64 u = (u64)r.unit;
     p.pending_used = (u == 2 && s->has_pending) ? 1 : 0;
     p.pending_val = (u32)s->pending;
     rs_status rc;
 
-    if (s->engine == RS_ENG_SFC64) {  // single stream: serial
+    if (is_serial(s->engine)) {  // sfc64 / sfc64simd single stream: no skip-ahead, serial
         p.n = n;
+        if (s->engine == RS_ENG_SFC64_SIMD) memcpy(p.lanes, s->state, sizeof p.lanes);
         DevResult *res = c.res;
         void *args[] = {&p, &res};
-        rc = launch(serial_kernel(r.family, r.fixed_mode), dim3(1), dim3(32), args, st);
+        rc = launch(serial_kernel(s->engine, r.family, r.fixed_mode), dim3(1), dim3(32), args, st);
         if (rc) return rc;
         if (sync) {
             CK(cudaMemcpyAsync(c.res_host, c.res, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
@@ -1597,6 +1715,12 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
             chunks = 1;
             return RS_OK;
         }
+        if (rs::simd_engine(s->engine)) {
+            if ((rc = launch_simd(c, p, r.fixed_mode, st))) return rc;
+            E = n;
+            chunks = 1;
+            return RS_OK;
+        }
         const void *fn = fixed_kernel(s->engine, r.fixed_mode);
         rc = plan_segments(c, p, p.weng ? p.weng : 1, 64, occupancy(fn), st);
         if (rc) return rc;
@@ -1626,11 +1750,14 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
         if (!first) {
             p.P = 0;
             p.pending_used = 0;
-            memcpy(p.base, s->state, sizeof p.base);
-            if (!rs::engine_advance_words(s->engine, p.base, (u128)origin)) {
+            u64 st32[32];
+            memcpy(st32, s->state, sizeof st32);
+            if (!rs::engine_advance_words(s->engine, st32, (u128)origin)) {
                 rs::set_error("cannot position engine");
                 return RS_ERR_INTERNAL;
             }
+            memcpy(p.base, st32, sizeof p.base);
+            memcpy(p.lanes, st32, sizeof p.lanes);
         }
         p.lp0 = lp0;
         p.n = need;
@@ -1805,7 +1932,7 @@ rs_status rs_fill(rs_stream *s, int32_t dist, const double *fparams, const uint6
     } else {
         E = Eu;
     }
-    if ((rc = apply_consumption(s, E, s->engine == RS_ENG_SFC64 ? c->res_host : nullptr))) return rc;
+    if ((rc = apply_consumption(s, E, is_serial(s->engine) ? c->res_host : nullptr))) return rc;
     if (odd) {
         u64 last = E - 1;
         u64 w = last < (u64)P ? pre_words[last] : s->buf[s->cursor - 1];

@@ -20,6 +20,7 @@ int state_words(int e) {
     case RS_ENG_X256PP: case RS_ENG_X256SS: case RS_ENG_PCG64: case RS_ENG_SFC64: return 4;
     case RS_ENG_PHILOX: return 6;
     case RS_ENG_RANLUX: return 9;
+    case RS_ENG_X256PP_SIMD: case RS_ENG_X256SS_SIMD: case RS_ENG_SFC64_SIMD: return 32;
     default: return 0;
     }
 }
@@ -27,12 +28,21 @@ int seed_words(int e) {
     switch (e) {
     case RS_ENG_X256PP: case RS_ENG_X256SS: case RS_ENG_PCG64: return 4;
     case RS_ENG_PHILOX: return 2;
-    case RS_ENG_SFC64: return 3;
+    case RS_ENG_SFC64: case RS_ENG_SFC64_SIMD: return 3;
     case RS_ENG_RANLUX: return 9;
+    case RS_ENG_X256PP_SIMD: case RS_ENG_X256SS_SIMD: return 4;
     default: return 0;
     }
 }
-int chunk(int e) { return e == RS_ENG_PHILOX ? 4 : e == RS_ENG_RANLUX ? 9 : 1; }
+int chunk(int e) {
+    switch (e) {
+    case RS_ENG_PHILOX: return 4;
+    case RS_ENG_RANLUX: return 9;
+    case RS_ENG_X256PP_SIMD: case RS_ENG_X256SS_SIMD: case RS_ENG_SFC64_SIMD: return 8;
+    default: return 1;
+    }
+}
+bool simd_engine(int e) { return e == RS_ENG_X256PP_SIMD || e == RS_ENG_X256SS_SIMD || e == RS_ENG_SFC64_SIMD; }
 bool known_engine(int e) { return state_words(e) > 0; }
 bool device_engine(int e) { return known_engine(e); }
 
@@ -272,11 +282,25 @@ void engine_generate(int e, uint64_t *s, uint64_t *out, int n) {
         for (int c = 0; c < n / 9; c++) { rlx_mulmod(s, A, s); memcpy(out + 9 * c, s, 72); }
         break;
     }
+    case RS_ENG_X256PP_SIMD: case RS_ENG_X256SS_SIMD: case RS_ENG_SFC64_SIMD: {
+        // interleave.py:71-76: word i = lane (i mod 8) at step i / 8; state is lane-major
+        int base = e == RS_ENG_X256PP_SIMD ? RS_ENG_X256PP : e == RS_ENG_X256SS_SIMD ? RS_ENG_X256SS : RS_ENG_SFC64;
+        uint64_t w[1];
+        for (int i = 0; i < n; i++) {
+            engine_generate(base, s + 4 * (i & 7), w, 1);
+            out[i] = w[0];
+        }
+        break;
+    }
     }
 }
 
 bool engine_advance_words(int e, uint64_t *s, u128 words) {
     switch (e) {
+    case RS_ENG_X256PP_SIMD: case RS_ENG_X256SS_SIMD:  // every lane advances words/8 steps
+        if (words % 8) return false;
+        for (int k = 0; k < 8; k++) x256_advance(s + 4 * k, words / 8);
+        return true;
     case RS_ENG_X256SS: case RS_ENG_X256PP: x256_advance(s, words); return true;
     case RS_ENG_PCG64: pcg_advance(s, words); return true;
     case RS_ENG_PHILOX:
@@ -326,8 +350,32 @@ void seed_words_fe128(const uint64_t *ent, int nent, const uint64_t *spawn, int 
     }
 }
 
+// lanes of the xoshiro interleaved engines: lane k = base jumped k * 2^253 (interleave.py:201-208)
+static void x256_simd_lanes(uint64_t *s) {
+    for (int k = 1; k < 8; k++) mat_vec(x256_pow2(253), s + 4 * (k - 1), s + 4 * k);
+}
+// sfc64 lanes: the Weyl counter offset by k * 2^61 (interleave.py:225-228)
+static void sfc_simd_lanes(uint64_t *s) {
+    for (int k = 1; k < 8; k++) {
+        memcpy(s + 4 * k, s, 24);
+        s[4 * k + 3] = s[3] + (uint64_t)k * (1ULL << 61);
+    }
+}
+void engine_simd_from_base(int e, uint64_t *s) {
+    if (e == RS_ENG_SFC64_SIMD) sfc_simd_lanes(s);
+    else x256_simd_lanes(s);
+}
+
 void engine_seed_from(int e, const uint64_t *w, uint64_t *s) {
     switch (e) {
+    case RS_ENG_X256PP_SIMD: case RS_ENG_X256SS_SIMD:  // interleave.py:127-130
+        engine_seed_from(RS_ENG_X256PP, w, s);
+        x256_simd_lanes(s);
+        break;
+    case RS_ENG_SFC64_SIMD:  // interleave.py:212-215
+        engine_seed_from(RS_ENG_SFC64, w, s);
+        sfc_simd_lanes(s);
+        break;
     case RS_ENG_X256PP: case RS_ENG_X256SS:  // xorfam.py:66-70
         memcpy(s, w, 32);
         if (!(s[0] | s[1] | s[2] | s[3])) s[0] = 1;
@@ -386,6 +434,12 @@ rs_status rs_engine_check_state(int32_t e, const uint64_t *w) {
             set_error(std::string("all-zero state is invalid for ") + (e == RS_ENG_X256PP ? "x256++" : "x256**"));
             return RS_ERR_VALUE;
         }
+    } else if (e == RS_ENG_X256PP_SIMD || e == RS_ENG_X256SS_SIMD) {  // interleave.py:120-123
+        for (int k = 0; k < 8; k++)
+            if (!(w[4 * k] | w[4 * k + 1] | w[4 * k + 2] | w[4 * k + 3])) {
+                set_error("lane " + std::to_string(k) + " state must not be all zero");
+                return RS_ERR_VALUE;
+            }
     } else if (e == RS_ENG_PCG64) {
         if (!(w[2] & 1)) { set_error("pcg64 increment must be odd"); return RS_ERR_VALUE; }
     } else if (e == RS_ENG_RANLUX) {
@@ -417,6 +471,13 @@ rs_status rs_engine_jump(int32_t e, uint64_t *state, int32_t k) {
         memcpy(state, o, 32);
         break;
     }
+    case RS_ENG_X256PP_SIMD: case RS_ENG_X256SS_SIMD:  // per-lane jump, interleave.py:132-139
+        for (int l = 0; l < 8; l++) {
+            uint64_t o[4];
+            mat_vec(x256_pow2(k), state + 4 * l, o);
+            memcpy(state + 4 * l, o, 32);
+        }
+        break;
     case RS_ENG_PCG64:
         if (k >= 128) { uint64_t keep[4]; memcpy(keep, state, 32); (void)keep; break; }  // 2^k = 0 mod 2^128
         pcg_advance(state, (u128)1 << k);

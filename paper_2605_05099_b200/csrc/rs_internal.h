@@ -19,6 +19,8 @@ int state_words(int eng);
 int seed_words(int eng);
 int chunk(int eng);
 bool known_engine(int eng);
+bool simd_engine(int eng);
+void engine_simd_from_base(int eng, uint64_t *state);  // lanes 1..7 from lane 0
 bool device_engine(int eng);
 
 // ---- GF(2) 256x256 matrices for the xoshiro256 linear step (jumps.py:93-126 restated

@@ -78,6 +78,10 @@ class Engine:
             self.s = [0, 0, 0, 1]
         elif eid == "ranlux++":
             self.s[0] = 1
+        elif eid in ("x256++simd", "x256**simd"):  # lane k = [4k+1, 4k+2, 4k+3, 4k+4]
+            self.s = [4 * k + w + 1 for k in range(8) for w in range(4)]
+        elif eid == "sfc64simd":  # lanes from a default sfc64 (a=b=c=0, w=1), counters + k*2^61
+            self.s = [v for k in range(8) for v in (0, 0, 0, (1 + k * (1 << 61)) & MASK64)]
 
     def get_state(self):
         return list(self.s)
@@ -91,13 +95,13 @@ class Engine:
 
     def seed_from(self, words):
         w = _lib.u64_array(list(words)[:16], 16)
-        out = _lib.u64_array([], 9)
+        out = _lib.u64_array([], 32)
         _lib.check(_lib.lib.rs_engine_seed_from(self.native, w, out))
         self.s = [int(out[i]) for i in range(self.STATE_WORDS)]
 
     def generate(self, n):
         n = int(n)
-        st = _lib.u64_array(self.s, 9)
+        st = _lib.u64_array(self.s, 32)
         out = (_lib.ctypes.c_uint64 * max(1, n))()
         _lib.check(_lib.lib.rs_engine_generate(self.native, st, out, n))
         self.s = [int(st[i]) for i in range(self.STATE_WORDS)]
@@ -118,8 +122,15 @@ class Engine:
     def set_abc(self, words):  # sfc.py:38-43: (a, b, c), w = 0, 18-step warmup
         if len(words) != 3:
             raise ValueError("sfc64 stream selector is 3 words (a, b, c)")
-        self.s = [int(w) & MASK64 for w in words] + [0]
-        self.generate(18)
+        base = [int(w) & MASK64 for w in words] + [0]
+        st = _lib.u64_array(base, 32)
+        out = (_lib.ctypes.c_uint64 * 18)()
+        _lib.check(_lib.lib.rs_engine_generate(NATIVE_ID["sfc64"], st, out, 18))
+        a, b, c, w = (int(st[i]) for i in range(4))
+        if self.ID == "sfc64simd":  # interleave.py:217-228: lanes offset the counter by k*2^61
+            self.s = [v for k in range(8) for v in (a, b, c, (w + k * (1 << 61)) & MASK64)]
+        else:
+            self.s = [a, b, c, w]
 
 
 def engine_class_info():
@@ -131,7 +142,8 @@ def make(selector=None):
     row = next(r for r in _REGISTRY if r[0] == eid)
     if not _lib.lib.rs_engine_supported(row[9]):
         raise NotImplementedError(
-            "engine %r is not on the B200 fill path (supported: x256**, x256++, pcg64, philox, sfc64, ranlux++)"
+            "engine %r is not on the B200 fill path (supported: x256**, x256++, pcg64, philox, sfc64, ranlux++, "
+            "x256++simd, x256**simd, sfc64simd)"
             % eid)
     return Engine(*row)
 

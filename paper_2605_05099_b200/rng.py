@@ -25,7 +25,7 @@ from .buffer import CAPACITY, WordBuffer
 
 MASK64 = 0xFFFFFFFFFFFFFFFF
 
-_POLY_JUMP = {"x256++", "x256**"}
+_POLY_JUMP = {"x256++", "x256**", "x256++simd", "x256**simd"}
 STANDARD_JUMPS = (32, 64, 96, 128, 192)  # jumps.py:24
 _STREAM_METHODS = {  # rng.py:27-35
     "pcg64": ("set_inc", 2),
@@ -187,7 +187,7 @@ class Rng:
                 raise ValueError("%s jump exponent must be one of %s" % (eid, STANDARD_JUMPS))
         else:
             raise ValueError("jump unsupported for engine %s" % eid)
-        st = _lib.u64_array(self.engine.s, 9)
+        st = _lib.u64_array(self.engine.s, 32)
         _lib.check(_lib.lib.rs_engine_jump(self.engine.native, st, k))
         self.engine.s = [int(st[i]) for i in range(self.engine.STATE_WORDS)]
         self.buffer.reset()
@@ -197,7 +197,7 @@ class Rng:
         if self.engine_id != "pcg64":
             raise ValueError("advance unsupported for engine %s" % self.engine_id)
         d = int(delta) & ((1 << 128) - 1)
-        st = _lib.u64_array(self.engine.s, 9)
+        st = _lib.u64_array(self.engine.s, 32)
         _lib.check(_lib.lib.rs_pcg_advance(st, d & MASK64, d >> 64))
         self.engine.s = [int(st[i]) for i in range(4)]
         self.buffer.reset()

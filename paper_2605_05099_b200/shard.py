@@ -16,7 +16,7 @@ def shard_rng(engine, seed, rank, words_per_rank, spawn_key=(), full_mantissa=Fa
     r.set_full_mantissa(full_mantissa)
     off = int(rank) * int(words_per_rank)
     if off:
-        st = _lib.u64_array(r.engine.s, 9)
+        st = _lib.u64_array(r.engine.s, 32)
         _lib.check(_lib.lib.rs_engine_advance_words(r.engine.native, st, off & (2 ** 64 - 1), off >> 64))
         r.engine.s = [int(st[i]) for i in range(r.engine.STATE_WORDS)]
     return r

@@ -102,9 +102,12 @@ for m in (6, 1000003, (1 << 63) + 1):
         case("c5b_sfc64_b%d_j%d" % (m, j), "sfc64", [31], "uint64", {"b": m}, 4096, spawn=[j])
 case("extra_ranlux_raw", "ranlux++", [12345], "uint64", {}, 1 << 14, keep=False)
 case("extra_ranlux_raw_small", "ranlux++", [12345], "uint64", {}, 999)
+# the library default engine (create() with no name): x256++simd
+case("default_engine_raw", None, [2024], "uint64", {}, 1 << 16, keep=False)
+case("default_engine_norm", None, [2024], "norm", {}, 1 << 16, keep=False)
 
 # edge cases: empty / single / parameters / modes / mid-buffer starts
-ENG = ("x256**", "x256++", "pcg64", "philox", "sfc64", "ranlux++")
+ENG = ("x256**", "x256++", "pcg64", "philox", "sfc64", "ranlux++", "x256++simd", "x256**simd", "sfc64simd")
 for e in ENG:
     tag = e.replace("+", "p").replace("*", "s")
     case("edge_%s_n0" % tag, e, [5], "norm", {}, 0)
@@ -137,7 +140,7 @@ DERIVED = [("unif", {"a": -2.0, "b": 3.0}), ("unif", {}), ("uniff", {"a": -2.0, 
            ("int", {}), ("int", {"m": -(1 << 31), "n": 0}), ("long_long", {"m": -10 ** 15, "n": 10 ** 18}),
            ("long_long", {}), ("long_long", {"m": 7, "n": 7 + (1 << 40) - 1})]
 TRANSFORMED = ("lognormal", "gumbel", "pareto", "weibull", "gpd")
-for e in ("x256**", "pcg64", "philox", "sfc64", "ranlux++"):
+for e in ("x256**", "pcg64", "philox", "sfc64", "ranlux++", "x256++simd"):
     tag = e.replace("+", "p").replace("*", "s")
     for i, (dist, params) in enumerate(DERIVED):
         case("derived_%s_%s_%d" % (tag, dist, i), e, [100 + i], dist, params, 1500, pre=[("u32", 1)],

@@ -14,7 +14,7 @@ from conftest import golden_params, is_vectorized, vec_close
 
 pytestmark = pytest.mark.gpu
 
-ENGINES = ("x256**", "x256++", "pcg64", "philox", "sfc64", "ranlux++")
+ENGINES = ("x256**", "x256++", "pcg64", "philox", "sfc64", "ranlux++", "x256++simd", "x256**simd", "sfc64simd")
 
 
 def _h(ws):
@@ -54,7 +54,7 @@ def test_golden_fills(golden, golden_arrays):
     """Every reference-generated case (BASELINE configs at prefix sizes + edge cases)."""
     bad = []
     for rec in golden["fills"]:
-        if rec["engine"] not in ENGINES:
+        if (rec["engine"] or "x256++simd") not in ENGINES:
             continue
         r = state_io.create(rec["engine"], seed=rec["seed"], spawn_key=tuple(rec["spawn"]))
         r.set_full_mantissa(rec["full_mantissa"])
@@ -103,6 +103,11 @@ CASES = [
     ("philox", "uint64", {"b": 1 << 40}, 1 << 20),
     ("sfc64", "norm", {}, 1 << 16),
     ("sfc64", "uint64", {"b": 6}, 1 << 16),
+    ("x256++simd", "uint64", {}, (1 << 22) + 5),
+    ("x256**simd", "u01f", {}, (1 << 21) + 3),
+    ("x256++simd", "norm", {}, 1 << 21),
+    ("x256**simd", "gamma", {"alpha": 0.4}, 1 << 19),
+    ("sfc64simd", "norm", {}, 1 << 14),
 ]
 
 
@@ -170,7 +175,7 @@ def test_streams_half_and_transform_families():
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 35, 36, 37, 143, 144, 145, 1000, 4097, 65536 + 7])
-@pytest.mark.parametrize("engine", ["x256**", "pcg64", "philox", "ranlux++"])
+@pytest.mark.parametrize("engine", ["x256**", "pcg64", "philox", "ranlux++", "x256++simd"])
 def test_small_and_ragged(engine, n):
     for dist, params in (("uint64", {}), ("u01f", {}), ("norm", {}), ("gamma", {"alpha": 0.7}),
                          ("uint64", {"b": 3}), ("normf", {}), ("uint32", {"b": 3}), ("int", {}), ("uniff", {})):

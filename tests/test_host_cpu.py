@@ -41,7 +41,7 @@ def test_catalogue_and_registry():
     assert engines.normalize(None) == engines.normalize("0") == engines.normalize("") == "x256++simd"
     with pytest.raises(engines.UnknownEngineError):
         engines.normalize("nope")
-    for e in ("x256**", "x256++", "pcg64", "philox", "sfc64", "ranlux++"):
+    for e in ("x256**", "x256++", "pcg64", "philox", "sfc64", "ranlux++", "x256++simd", "x256**simd", "sfc64simd"):
         assert engines.supported(e)
     with pytest.raises(NotImplementedError):
         engines.make("chacha20")
@@ -89,7 +89,8 @@ def test_jumps_and_advance(golden):
         state_io.create("x256**", seed=[1]).jump(33)
 
 
-@pytest.mark.parametrize("engine", ["x256**", "x256++", "pcg64", "philox", "sfc64", "ranlux++"])
+@pytest.mark.parametrize("engine", ["x256**", "x256++", "pcg64", "philox", "sfc64", "ranlux++", "x256++simd",
+                                    "x256**simd", "sfc64simd"])
 def test_scalar_draws_match_oracle(engine):
     r = state_io.create(engine, seed=[4242])
     o = O.OracleRng(engine, seed=[4242])
@@ -180,3 +181,40 @@ def test_n_zero_is_a_no_op():
     out = r.fill("norm", {"var": -5}, 0)  # the reference validates nothing for n == 0
     assert out.numel() == 0 if hasattr(out, "numel") else len(out) == 0
     assert r.get_state() == st and r.buffer.capture() == snap
+
+
+def test_interleaved_lanes_are_jumped_scalar_lanes():
+    """interleave.py:9-13 / pkg/tests/test_engines_kat.py:54-98: lane k = base jumped k*2^253."""
+    for simd, base in (("x256++simd", "x256++"), ("x256**simd", "x256**")):
+        r = engines.make(simd)
+        r.seed_from([11, 22, 33, 44])
+        b = engines.make(base)
+        b.seed_from([11, 22, 33, 44])
+        lanes = []
+        st = b.get_state()
+        for _ in range(8):
+            lane = engines.make(base)
+            lane.set_state(st)
+            lanes.append(lane.generate(25))
+            s = _lib.u64_array(st, 32)
+            _lib.check(_lib.lib.rs_engine_jump(engines.NATIVE_ID[base], s, 253))
+            st = [int(s[i]) for i in range(4)]
+        assert r.generate(200) == [lanes[k][i] for i in range(25) for k in range(8)]
+    r = engines.make("sfc64simd")
+    r.seed_from([5, 6, 7])
+    s = engines.make("sfc64")
+    s.seed_from([5, 6, 7])
+    a, b_, c, w = s.get_state()
+    lanes = []
+    for k in range(8):
+        lane = engines.make("sfc64")
+        lane.set_state([a, b_, c, (w + k * (1 << 61)) & (2 ** 64 - 1)])
+        lanes.append(lane.generate(25))
+    assert r.generate(200) == [lanes[k][i] for i in range(25) for k in range(8)]
+
+
+def test_default_engine_is_x256pp_simd():
+    r = state_io.create(seed=[2024])
+    assert r.engine_id == "x256++simd"
+    o = O.OracleRng("x256++simd", seed=[2024])
+    assert r.get_state() == o.get_state()

@@ -86,7 +86,7 @@ def _fill_cases(golden, large):
 
 
 def _check_fill(rec, golden_arrays):
-    o = O.OracleRng(rec["engine"], seed=rec["seed"], spawn_key=tuple(rec["spawn"]),
+    o = O.OracleRng(rec["engine"] or "x256++simd", seed=rec["seed"], spawn_key=tuple(rec["spawn"]),
                     full_mantissa=rec["full_mantissa"])
     assert o.get_state() == _h(rec["start_state"])
     _run_pre(o, rec["pre"])
