@@ -624,6 +624,115 @@ RS_DEV double std_exp_f(S &s, const ZigCtxF &z) {
     }
 }
 
+// ----------------------------------------------------------------------------- word-level machines
+// The same ziggurat samplers restated one word at a time (states: 0 start, 1 slow
+// second word, 2/3 tail pairs). In a SIMT warp every lane then consumes exactly one
+// word per step, so the engine step is never inside a divergent branch -- only the
+// rare slow/tail decision is (1.5 % of normal, 2.2 % of exponential words).
+struct ZigWM {
+    u32 st, idx;
+    u64 rabs;
+    u32 neg;
+    double xx;
+};
+
+RS_DEV bool norm_rare(ZigWM &m, u64 w, const ZigCtx &z, Tally &t, double &out) {
+    if (m.st == 1) {  // second word of the slow path (continuous.py:59-68)
+        m.st = 0;
+        u64 yv = w >> 12;
+        int idx = (int)m.idx;
+        double x = (double)m.rabs * z.fast[idx].w;
+        u64 K = __ldg(&z.slow->k[idx]);
+        u64 lo, hi;
+        zig_lhs(yv, (1ULL << 52) - K, m.rabs - K, lo, hi);
+        bool acc = lt128(lo, hi, __ldg(&z.slow->ta_lo[idx]), __ldg(&z.slow->ta_hi[idx]));
+        if (!acc && !lt128(__ldg(&z.slow->tr_lo[idx]), __ldg(&z.slow->tr_hi[idx]), lo, hi)) {
+            t.norm_pdf++;
+            double fi = __ldg(&z.slow->f[idx]), fim1 = __ldg(&z.slow->f[idx - 1]);
+            double y = fi + ((double)yv * 2.220446049250313e-16) * (fim1 - fi);
+            acc = y < det_exp_dev(-0.5 * x * x);
+        }
+        if (acc) out = m.neg ? -x : x;
+        return acc;
+    }
+    if (m.st == 2) {  // tail: xx (continuous.py:52-58)
+        m.xx = -dbl(RS_NOR_INV_R_BITS) * det_log_dev(1.0 - u01_of(w, z.fm));
+        m.st = 3;
+        return false;
+    }
+    double yy = -det_log_dev(1.0 - u01_of(w, z.fm));
+    if (yy + yy > m.xx * m.xx) {
+        double r = dbl(RS_NOR_R_BITS) + m.xx;
+        out = m.neg ? -r : r;
+        m.st = 0;
+        return true;
+    }
+    m.st = 2;
+    return false;
+}
+
+// std_norm one word at a time; returns true when a sample completes (in out).
+// f = z.fast[w & 0xFF], loaded by the caller (batched loads overlap their latency)
+RS_DEV bool norm_feed(ZigWM &m, u64 w, ZigFast f, const ZigCtx &z, Tally &t, double &out) {
+    if (__builtin_expect(m.st == 0, 1)) {
+        t.norm_att++;
+        int idx = (int)(w & 0xFF);
+        u64 rabs = (w >> 9) & ((1ULL << 52) - 1);
+        if (rabs < f.k) {
+            double x = (double)rabs * f.w;
+            out = (w >> 8) & 1 ? -x : x;
+            return true;
+        }
+        m.idx = idx;
+        m.rabs = rabs;
+        m.neg = (u32)((w >> 8) & 1);
+        m.st = idx == 0 ? 2 : 1;
+        return false;
+    }
+    return norm_rare(m, w, z, t, out);
+}
+
+RS_DEV bool exp_rare(ZigWM &m, u64 w, const ZigCtx &z, Tally &t, double &out) {
+    if (m.st == 1) {  // continuous.py:83-93
+        m.st = 0;
+        u64 yv = w >> 12;
+        int idx = (int)m.idx;
+        double x = (double)m.rabs * z.fast[idx].w;
+        u64 K = __ldg(&z.slow->k[idx]);
+        u64 lo, hi;
+        zig_lhs(yv, (1ULL << 53) - K, m.rabs - K, lo, hi);
+        bool acc = lt128(lo, hi, __ldg(&z.slow->ta_lo[idx]), __ldg(&z.slow->ta_hi[idx]));
+        if (!acc && !lt128(__ldg(&z.slow->tr_lo[idx]), __ldg(&z.slow->tr_hi[idx]), lo, hi)) {
+            t.exp_pdf++;
+            double fe = __ldg(&z.slow->f[idx]), fem1 = __ldg(&z.slow->f[idx - 1]);
+            double y = fe + ((double)yv * 2.220446049250313e-16) * (fem1 - fe);
+            acc = y < det_exp_dev(-x);
+        }
+        if (acc) out = x;
+        return acc;
+    }
+    m.st = 0;  // tail (continuous.py:82): one uniform
+    out = dbl(RS_EXP_R_BITS) - det_log_dev(1.0 - u01_of(w, z.fm));
+    return true;
+}
+
+RS_DEV bool exp_feed(ZigWM &m, u64 w, ZigFast f, const ZigCtx &z, Tally &t, double &out) {
+    if (__builtin_expect(m.st == 0, 1)) {
+        t.exp_att++;
+        int idx = (int)(w & 0xFF);
+        u64 rabs = (w >> 8) & ((1ULL << 53) - 1);
+        if (rabs < f.k) {
+            out = (double)rabs * f.w;
+            return true;
+        }
+        m.idx = idx;
+        m.rabs = rabs;
+        m.st = idx == 0 ? 2 : 1;
+        return false;
+    }
+    return exp_rare(m, w, z, t, out);
+}
+
 // ----------------------------------------------------------------------------- distributions
 // A Dist draws one sample per call to sample(s, t). Families share a kernel and pick
 // the law with a (warp-uniform) kind, which keeps the number of kernel instantiations
@@ -638,6 +747,15 @@ struct DistNorm {  // continuous.py:157-158 (norm), :176-177 (lognormal), :281-2
     int kind;
     // a skew-normal sample is a pair of normals: the phase-1 parse starts with its second one
     RS_DEV bool paired() const { return kind == NK_SKEW; }
+    RS_DEV bool word_level() const { return kind != NK_SKEW; }
+    RS_DEV double finish(double v) const {
+        if (kind == NK_STD) return v;
+        double r = a + b * v;
+        return kind == NK_LOGNORMAL ? det_exp_dev(r) : r;
+    }
+    RS_DEV ZigFast strip(u64 w) const { return z.fast[w & 0xFF]; }
+    RS_DEV bool feed(ZigWM &m, u64 w, ZigFast f, Tally &t, double &out) const { return norm_feed(m, w, f, z, t, out); }
+    RS_DEV bool feed(ZigWM &m, u64 w, Tally &t, double &out) const { return norm_feed(m, w, strip(w), z, t, out); }
     template <class S> RS_DEV void skip_second(S &s, Tally &t) const { std_norm(s, z, t); }
     template <class S> RS_DEV double sample(S &s, Tally &t) const {
         double v = std_norm(s, z, t);
@@ -659,6 +777,18 @@ struct DistExp {  // continuous.py:165-169 (exp), :252-254 (pareto), :257-266 (g
     int kind;
     RS_DEV bool paired() const { return false; }
     template <class S> RS_DEV void skip_second(S &, Tally &) const {}
+    RS_DEV bool word_level() const { return true; }
+    RS_DEV double finish(double e) const {
+        if (kind == EK_EXP) return a * e;
+        if (kind == EK_PARETO) return b * det_exp_dev(e / a);
+        if (kind == EK_WEIBULL) return b * det_exp_dev(det_log_dev(e) / a);
+        if (a == 0.0) return b + c * e;
+        double p = det_exp_dev(e * fabs(a));
+        return a > 0.0 ? b + c * (p - 1.0) / a : b - c * (1.0 - 1.0 / p) / a;
+    }
+    RS_DEV ZigFast strip(u64 w) const { return z.fast[w & 0xFF]; }
+    RS_DEV bool feed(ZigWM &m, u64 w, ZigFast f, Tally &t, double &out) const { return exp_feed(m, w, f, z, t, out); }
+    RS_DEV bool feed(ZigWM &m, u64 w, Tally &t, double &out) const { return exp_feed(m, w, strip(w), z, t, out); }
     template <class S> RS_DEV double sample(S &s, Tally &t) const {
         double e = std_exp(s, z, t);
         if (kind == EK_EXP) return a * e;

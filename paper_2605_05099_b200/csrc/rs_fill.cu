@@ -120,12 +120,25 @@ template <> struct EngOf<RS_ENG_SFC64_SIMD> { typedef EngSfcSimd type; };
 // both parse passes read them back instead of regenerating them.
 constexpr int RS_ENG_MEM = 100;
 __device__ u32 g_mem_overrun;
-struct EngMem {
+struct EngMem {  // reads its (per-lane sequential) words 32 bytes at a time
     const u64 *w;
     u64 idx, nw;
+    u64 b0, b1, b2, b3;
+    int have;
     __device__ __forceinline__ u64 next() {
-        if (idx >= nw) { g_mem_overrun = 1; return 0; }
-        return __ldg(w + idx++);
+        if (have == 0) {
+            u64 g = idx & ~3ULL;
+            if (g >= nw) { g_mem_overrun = 1; return 0; }
+            asm volatile("ld.global.nc.v4.b64 {%0, %1, %2, %3}, [%4];"
+                         : "=l"(b0), "=l"(b1), "=l"(b2), "=l"(b3) : "l"(w + g));
+            have = 4;
+            for (u64 j = g; j < idx; j++) { b0 = b1; b1 = b2; b2 = b3; have--; }
+        }
+        u64 r = b0;
+        b0 = b1; b1 = b2; b2 = b3;
+        have--;
+        idx++;
+        return r;
     }
 };
 template <> struct EngOf<RS_ENG_MEM> { typedef EngMem type; };
@@ -164,6 +177,7 @@ __device__ __forceinline__ void make_engine(const FillPlan &p, u32 t, typename E
         e.w = p.words;
         e.idx = (u64)t * p.L;
         e.nw = p.nwords;
+        e.have = 0;
     }
 }
 
@@ -357,6 +371,62 @@ constexpr int minb(int E, int D) {
     return D == FAM_GAMMA ? 2 : (D == FAM_LEMIRE || D == FAM_U32) ? 4 : 3;
 }
 
+// ----------------------------------------------------------------------------- word-level drivers
+// Samples that start before `end` (count) / the next `kmax` samples (emit) with one
+// word per lane per step. The buffered prefix (thread 0 of the first chunk only) is
+// consumed in a preamble so the steady-state loop reads the engine directly and
+// tracks its position with 32-bit counters.
+template <class D, class SRC>
+__device__ __forceinline__ u64 wl_count(const D &d, SRC &s, u64 end, Tally &tl) {
+    ZigWM m;
+    m.st = 0;
+    bool bnd = true;
+    u64 c = 0;
+    while (s.npre > 0 && !(bnd && s.pos >= end)) {
+        double z;
+        bnd = d.feed(m, s.next(), tl, z);
+        c += bnd;
+    }
+    u32 left = s.pos < end ? (u32)(end - s.pos) : 0u, used = 0, cc = 0;
+    // 4 words per step: the engine chain and the 4 strip loads overlap; words generated
+    // past the exit are dropped (only the position matters)
+    while (!(bnd && used >= left)) {
+        u64 w[4];
+        ZigFast f[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) w[k] = s.e.next();
+#pragma unroll
+        for (int k = 0; k < 4; k++) f[k] = d.strip(w[k]);
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            if (bnd && used >= left) break;
+            double z;
+            bnd = d.feed(m, w[k], f[k], tl, z);
+            used++;
+            cc += bnd;
+        }
+    }
+    s.pos += used;
+    return c + cc;
+}
+template <class D, class SRC, class W>
+__device__ __forceinline__ void wl_emit(const D &d, SRC &s, u64 kmax, W &wr, Tally &tl) {
+    ZigWM m;
+    m.st = 0;
+    u64 k = 0;
+    while (s.npre > 0 && k < kmax) {
+        double z;
+        if (d.feed(m, s.next(), tl, z)) { wr.put(d.finish(z)); k++; }
+    }
+    u32 left = (u32)(kmax - k), used = 0;
+    while (left) {
+        double z;
+        used++;
+        if (d.feed(m, s.e.next(), tl, z)) { wr.put(d.finish(z)); left--; }
+    }
+    s.pos += used;
+}
+
 // ----------------------------------------------------------------------------- two-pass parse
 // count: samples that START inside [seg_start, seg_end) and the exit (first sample
 // boundary at or beyond seg_end), parsing from seg_start as if it were a boundary.
@@ -387,10 +457,18 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_count(const __grid_consta
             c += bnd;
         }
     } else {
-        while (s.pos < end) {
-            d.sample(s, tl);
-            c++;
+        bool done = false;
+        if constexpr (D == FAM_NORM || D == FAM_EXP) {
+            if (d.word_level()) {  // one word per lane per step (uniform engine step)
+                c = wl_count(d, s, end, tl);
+                done = true;
+            }
         }
+        if (!done)
+            while (s.pos < end) {
+                d.sample(s, tl);
+                c++;
+            }
         if (d.paired()) {
             typename SrcOf<E, D>::type s1;
             make_src<E>(p, t, seg_start(p, t), s1);
@@ -521,7 +599,15 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constan
                     if (ok) { wr.put(v); k++; }
                 }
             } else {
-                for (u64 k = 0; k < kmax; k++) wr.put(d.sample(s, tl));
+                bool done = false;
+                if constexpr (D == FAM_NORM || D == FAM_EXP) {
+                    if (d.word_level()) {
+                        wl_emit(d, s, kmax, wr, tl);
+                        done = true;
+                    }
+                }
+                if (!done)
+                    for (u64 k = 0; k < kmax; k++) wr.put(d.sample(s, tl));
             }
             wr.finish();
             if (o + kmax == p.n) res->end_pos = s.pos;
