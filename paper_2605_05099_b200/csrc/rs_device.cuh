@@ -66,21 +66,6 @@ struct EngPcg {  // pcg.py:25-39 (DXSM of the pre-step state; 64-bit "cheap" mul
     }
 };
 
-// 64x64 -> 128 product with four 32x32->64 multiply-adds (IMAD.WIDE.U32). Both
-// carries are folded into the last addend: a1*b1 + hi(p1) + hi(p2) < 2^64, so the
-// only extra work is one 64-bit add on the ALU pipe (the IMAD pipe is the bound).
-RS_DEV void mul64x64(u64 a, u64 b, u64 &lo, u64 &hi) {
-    u32 a0 = (u32)a, a1 = (u32)(a >> 32), b0 = (u32)b, b1 = (u32)(b >> 32);
-    u64 p0, p1, p2, p3;
-    asm("mul.wide.u32 %0, %1, %2;" : "=l"(p0) : "r"(a0), "r"(b0));
-    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p1) : "r"(a1), "r"(b0), "l"(p0 >> 32));
-    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p2) : "r"(a0), "r"(b1), "l"((u64)(u32)p1));
-    u64 t = (p1 >> 32) + (p2 >> 32);
-    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p3) : "r"(a1), "r"(b1), "l"(t));
-    lo = (p2 << 32) | (u64)(u32)p0;
-    hi = p3;
-}
-
 // the same product as a 32-bit multiply-add carry chain (IMAD / IMAD.HI with .X)
 RS_DEV void mul64x64_cc(u64 a, u64 b, u64 &lo, u64 &hi) {
     u32 a0 = (u32)a, a1 = (u32)(a >> 32), b0 = (u32)b, b1 = (u32)(b >> 32);
@@ -102,6 +87,24 @@ RS_DEV void mul64x64_cc(u64 a, u64 b, u64 &lo, u64 &hi) {
     hi = ((u64)r3 << 32) | r2;
 }
 
+RS_DEV u64 mulw(u32 a, u32 b) {
+    u64 r;
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(r) : "r"(a), "r"(b));
+    return r;
+}
+// 64x64 -> 128 product: four 32x32->64 products (IMAD.WIDE.U32, 4 cycles each on the
+// fmaheavy pipe -- 16 cycles per product is the floor) and the column sums as 64-bit
+// adds of zero-extended halves, which ptxas splits between the ALU pipe (IADD3 with
+// two carries) and the FMA pipe. Measured the fastest of five formulations on B200
+// (profiles/README.md, round 1: Philox u01 2^30 3.82 -> 3.69 ms).
+RS_DEV void mul64x64(u64 a, u64 b, u64 &lo, u64 &hi) {
+    u32 a0 = (u32)a, a1 = (u32)(a >> 32), b0 = (u32)b, b1 = (u32)(b >> 32);
+    u64 p00 = mulw(a0, b0), p01 = mulw(a0, b1), p10 = mulw(a1, b0), p11 = mulw(a1, b1);
+    u64 mid = (p00 >> 32) + (u64)(u32)p01 + (u64)(u32)p10;
+    lo = (mid << 32) | (u64)(u32)p00;
+    hi = p11 + (p01 >> 32) + (p10 >> 32) + (mid >> 32);
+}
+
 RS_DEV void philox4x64_10(u64 c0, u64 c1, u64 c2, u64 c3, u64 k0, u64 k1, u64 &o0, u64 &o1, u64 &o2, u64 &o3) {
     // counter.py:83-96
 #pragma unroll
@@ -118,6 +121,7 @@ RS_DEV void philox4x64_10(u64 c0, u64 c1, u64 c2, u64 c3, u64 k0, u64 k1, u64 &o
 }
 
 // same bijection with the 10 round keys precomputed (read from the constant bank)
+// V = 0: mul64x64 (default); V = 1: the mad.cc-chain form (RS_PHILOX_VARIANT=1)
 template <int V = 0>
 RS_DEV void philox4x64_10_rk(u64 c0, u64 c1, u64 c2, u64 c3, const u64 *rk0, const u64 *rk1, u64 &o0, u64 &o1,
                              u64 &o2, u64 &o3) {
