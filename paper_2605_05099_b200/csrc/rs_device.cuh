@@ -934,6 +934,59 @@ struct VecWriter8 {
     }
 };
 
+// Writes one thread's contiguous output run [start, ...) in 32-byte groups: the
+// current group is staged in a per-thread shared-memory ring (slot-major, so a warp's
+// STS is conflict-free) and leaves as one STG.256 once full. Partial head/tail groups
+// (shared with the neighbouring runs) are written element by element. Unlike a
+// register array with a dynamic slot index, put() is branch-free apart from the flush.
+template <class T, int NT>
+struct RingWriter {
+    static constexpr int G = 32 / (int)sizeof(T);
+    T *abase;  // 32-byte aligned base
+    u64 vi;    // element index (from abase) of the current group
+    int slot, first;
+    T *ring;   // this thread's slot 0; slot k at ring[k * NT]
+    RS_DEV void init(T *out, u64 start, T *ring_) {
+        ring = ring_;
+        uintptr_t a = (uintptr_t)out;
+        abase = (T *)(a & ~(uintptr_t)31);
+        u64 s = start + (u64)((a & 31) / sizeof(T));
+        vi = s & ~(u64)(G - 1);
+        slot = (int)(s & (G - 1));
+        first = slot;
+    }
+    RS_DEV void put(T v) {
+        ring[slot * NT] = v;
+        if (++slot == G) flush_full();
+    }
+    RS_DEV void flush_full() {
+        T *p = abase + vi;
+        if (first == 0) {
+            u64 q[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                if constexpr (sizeof(T) == 8) {
+                    q[k] = *(const u64 *)&ring[k * NT];
+                } else {
+                    u64 lo = *(const u32 *)&ring[(2 * k) * NT], hi = *(const u32 *)&ring[(2 * k + 1) * NT];
+                    q[k] = lo | (hi << 32);
+                }
+            }
+            asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(q[0]), "l"(q[1]), "l"(q[2]),
+                         "l"(q[3]) : "memory");
+        } else {
+            for (int k = first; k < G; k++) p[k] = ring[k * NT];
+        }
+        first = 0;
+        slot = 0;
+        vi += G;
+    }
+    RS_DEV void finish() {
+        T *p = abase + vi;
+        for (int k = first; k < slot; k++) p[k] = ring[k * NT];
+    }
+};
+
 template <class T>
 struct ScalarWriter {
     T *ptr;

@@ -572,6 +572,7 @@ template <int E, int D>
 __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constant__ FillPlan p, const u32 *entry, const u64 *cnt,
                                                 const u64 *off, const u32 *ex, DevResult *res) {
     __shared__ ZigFast sm[256];
+    __shared__ __align__(16) unsigned char ring_sm[32 * BLOCK];
     stage_tables(p, sm);
     u32 t = blockIdx.x * BLOCK + threadIdx.x;
     Tally tl = {0, 0, 0, 0, 0};
@@ -588,8 +589,8 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constan
             typename DistOf<D>::type d;
             make_dist<D>(p, sm, d);
             typedef typename DistOf<D>::type::out_t T;
-            typename std::conditional<sizeof(T) == 8, VecWriter8<T>, ScalarWriter<T>>::type wr;
-            wr.init((T *)p.out, p.out0 + o);
+            RingWriter<T, BLOCK> wr;
+            wr.init((T *)p.out, p.out0 + o, (T *)ring_sm + threadIdx.x);
             if constexpr (D == FAM_LEMIRE || D == FAM_U32) {
                 for (u64 k = 0; k < kmax;) {
                     T v;
@@ -1077,8 +1078,9 @@ __global__ void __launch_bounds__(BLOCK) k_streams(const __grid_constant__ Strea
     DistArgs da{a.fp, a.ip, &a.ga, &a.gb, a.kind, a.fm, a.zslow, a.zslowf};
     make_dist_a<D>(da, sm, d);
     typedef typename DT::out_t T;
-    typename std::conditional<sizeof(T) == 8, VecWriter8<T>, ScalarWriter<T>>::type wr;
-    wr.init((T *)a.out, j * a.nper);
+    __shared__ __align__(16) unsigned char ring_sm[32 * BLOCK];
+    RingWriter<T, BLOCK> wr;
+    wr.init((T *)a.out, j * a.nper, (T *)ring_sm + threadIdx.x);
     Tally tl;
     if constexpr (D == FAM_LEMIRE) {
         for (u64 i = 0; i < a.nper;) {
