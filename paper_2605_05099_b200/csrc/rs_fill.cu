@@ -1586,12 +1586,16 @@ void fill_plan_common(FillPlan &p, DevCtx &c, const Resolved &r, int engine, int
 }
 
 // Segment geometry + per-engine jump tables for stride L (engine origin = p.base)
-rs_status plan_segments(DevCtx &c, FillPlan &p, u64 words, u64 Lmin, int occ, cudaStream_t st, bool tables = true) {
+rs_status plan_segments(DevCtx &c, FillPlan &p, u64 words, u64 Lmin, int occ, cudaStream_t st, bool tables = true,
+                        u64 align = 36) {
     // exactly one wave of resident threads: equal segments finish together
     u64 Tfull = (u64)c.sms * (u64)occ * BLOCK;
     u64 L = (words + Tfull - 1) / Tfull;
     if (L < Lmin) L = Lmin;
-    L = (L + 35) / 36 * 36;  // a whole number of philox blocks and ranlux chunks
+    // a whole number of philox blocks (4) and ranlux chunks (9); fixed fills pass
+    // align = 144 (also 16-word lines): every thread then has the same alignment
+    // prologue, so the lanes stay in phase (ranlux mulmods convergent)
+    L = (L + align - 1) / align * align;
     u64 T = (words + L - 1) / L;
     if (T < 1) T = 1;
     T = (T + BLOCK - 1) / BLOCK * BLOCK;
@@ -1728,7 +1732,7 @@ rs_status launch_raw_words(DevCtx &c, FillPlan &m, cudaStream_t st) {
         return launch(fn, dim3((unsigned)g), dim3(BLOCK), args, st);
     }
     const void *fn = fixed_kernel(m.engine, FX_RAW);
-    if ((rc = plan_segments(c, m, m.weng, 64, occupancy(fn), st))) return rc;
+    if ((rc = plan_segments(c, m, m.weng, 64, occupancy(fn), st, true, 144))) return rc;
     void *args[] = {&m};
     return launch(fn, dim3(m.T / BLOCK), dim3(BLOCK), args, st);
 }
@@ -1809,7 +1813,7 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
             return RS_OK;
         }
         const void *fn = fixed_kernel(s->engine, r.fixed_mode);
-        rc = plan_segments(c, p, p.weng ? p.weng : 1, 64, occupancy(fn), st);
+        rc = plan_segments(c, p, p.weng ? p.weng : 1, 64, occupancy(fn), st, true, 144);
         if (rc) return rc;
         void *args[] = {&p};
         rc = launch(fn, dim3(p.T / BLOCK), dim3(BLOCK), args, st);
