@@ -544,6 +544,25 @@ struct GammaPrm {
     int boost;         // alpha < 1: core runs gamma(alpha+1, 1), then the U^(1/alpha) boost
 };
 
+// gamma_core's exact acceptance test after the squeeze fails (continuous.py:199):
+//   det_log(u) < 0.5 zz + d - d v + d det_log(v).
+// Both sides are first estimated with the MUFU log (__logf: <= 2^-21.4 absolute on
+// [0.5, 2], 3 ulp elsewhere; plus 2^-24 from rounding the argument to f32). Outside a
+// band of 1e-5 (1 + |log u| + d (1 + |log v|)) -- 25x those bounds, far above the
+// double rounding of either side -- the estimate decides exactly as the exact
+// expression would; inside it (and for 0, NaN or f32-underflowing arguments, where
+// the comparisons fail) the exact det_log expression decides. This keeps the
+// ~10 % of attempts that miss the squeeze off the two-det_log divergent path.
+RS_DEV bool gamma_accept(double u, double zz, double v, const GammaPrm &g) {
+    double a = (double)__logf((float)u);
+    double lv = (double)__logf((float)v);
+    double b = 0.5 * zz + g.d - g.d * v + g.d * lv;
+    double m = 1e-5 * (1.0 + fabs(a) + g.d * (1.0 + fabs(lv))) + 1e-12 * (zz + g.d * v);
+    if (a < b - m) return true;
+    if (a > b + m) return false;
+    return det_log_dev(u) < 0.5 * zz + g.d - g.d * v + g.d * det_log_dev(v);
+}
+
 template <class S>
 RS_DEV double gamma_core(S &s, const ZigCtx &z, const GammaPrm &g, Tally &t) {
     while (true) {
@@ -557,7 +576,7 @@ RS_DEV double gamma_core(S &s, const ZigCtx &z, const GammaPrm &g, Tally &t) {
         double u = u01_of(s.next(), z.fm);
         double zz = zn * zn;
         if (u < 1.0 - 0.0331 * zz * zz) return g.td * v;
-        if (det_log_dev(u) < 0.5 * zz + g.d - g.d * v + g.d * det_log_dev(v)) return g.td * v;
+        if (gamma_accept(u, zz, v, g)) return g.td * v;
     }
 }
 

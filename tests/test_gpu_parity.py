@@ -345,10 +345,24 @@ def test_c3_full_2p28(engine):
                                          ("gamma", {"alpha": 2.5}), ("gamma", {"alpha": 10.0}),
                                          ("beta", {"a": 2.0, "b": 5.0})])
 def test_c4_full_2p26(dist, params):
-    n = 1 << 26
-    r = state_io.create("pcg64", seed=[99])
+    _full_vs_oracle("pcg64", 99, dist, params, 1 << 26)
+
+
+# gamma's acceptance screen (gamma_accept) scales its band with d: extreme shapes and
+# the gamma-derived laws at 2^24, every sample against the oracle
+@pytest.mark.slow
+@pytest.mark.parametrize("dist,params", [("gamma", {"alpha": 0.01}), ("gamma", {"alpha": 1000.0}),
+                                         ("gamma", {"alpha": 1e6, "theta": 3.0}), ("chi2", {"nu": 3.0}),
+                                         ("t", {"nu": 4.5}), ("f", {"nu1": 3.0, "nu2": 7.0}),
+                                         ("beta", {"a": 0.5, "b": 0.5})])
+def test_gamma_screen_2p24(dist, params):
+    _full_vs_oracle("x256**", 4242, dist, params, 1 << 24)
+
+
+def _full_vs_oracle(engine, seed, dist, params, n):
+    r = state_io.create(engine, seed=[seed])
     got = r.fill(dist, params, n).cpu().numpy()
-    o = O.OracleRng("pcg64", seed=[99])
+    o = O.OracleRng(engine, seed=[seed])
     ref = o.fill(dist, params, n)
     diff = np.nonzero(_bits(got) != _bits(ref))[0]
     assert len(diff) == 0, "first diff at %d" % diff[0]
