@@ -43,6 +43,12 @@ using rs::u128;
 namespace {
 
 constexpr int BLOCK = 256;
+// Gamma-family parses converge only after ~10^2 words, so the count
+// pass records where its parses put sample boundaries in the first BM_WORDS * 32
+// units of the segment; the fixup then re-parses from the true entry alone and looks
+// the meeting point up instead of re-running the speculative parses beside it.
+constexpr u32 BM_WORDS = 32;
+constexpr u64 BM_UNITS = 32 * BM_WORDS;
 constexpr int MAXLEV = 24;
 constexpr int CAP = RS_BUFFER_CAPACITY;
 
@@ -76,6 +82,7 @@ struct FillPlan {
     const u64 *x256_states;
     const u64 *words;             // materialized engine words (RS_ENG_MEM parse source)
     u64 nwords;
+    u32 *bm;                      // gamma family: count-pass boundary bitmaps (see BM_WORDS)
     const RsZigSlow *zslow;
     const ZigFast *zfast;
     const u64 *rlx_A;
@@ -428,6 +435,31 @@ __device__ __forceinline__ void wl_emit(const D &d, SRC &s, u64 kmax, W &wr, Tal
 }
 
 // ----------------------------------------------------------------------------- two-pass parse
+// boundary bitmap writer: bit q of the segment's map = a sample starts at start + q
+struct BmRec {
+    u32 *bm;  // [BM_WORDS][T]
+    u32 T, t;
+    u64 start;
+    u32 acc = 0, kw = 0;
+    __device__ __forceinline__ void put(u64 pos) {
+        u64 q = pos - start;
+        if (!bm || q >= BM_UNITS) return;
+        u32 k = (u32)(q >> 5);
+        while (kw < k) { bm[(size_t)kw * T + t] = acc; acc = 0; kw++; }
+        acc |= 1u << (q & 31);
+    }
+    __device__ __forceinline__ void close() {
+        if (!bm) return;
+        while (kw < BM_WORDS) { bm[(size_t)kw * T + t] = acc; acc = 0; kw++; }
+    }
+};
+// samples of a recorded parse that start before unit q (q < BM_UNITS)
+__device__ __forceinline__ u64 bm_rank(const u32 *bm, u32 T, u32 t, u64 q) {
+    u32 k = (u32)(q >> 5);
+    u64 r = 0;
+    for (u32 j = 0; j < k; j++) r += __popc(bm[(size_t)j * T + t]);
+    return r + __popc(bm[(size_t)k * T + t] & ((1u << (q & 31)) - 1u));
+}
 // count: samples that START inside [seg_start, seg_end) and the exit (first sample
 // boundary at or beyond seg_end), parsing from seg_start as if it were a boundary.
 // For paired samplers (beta, f, t, skew_normal: two sub-samples per sample) a parse
@@ -464,20 +496,36 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_count(const __grid_consta
                 done = true;
             }
         }
-        if (!done)
-            while (s.pos < end) {
-                d.sample(s, tl);
-                c++;
+        if (!done) {
+            if constexpr (D == FAM_GAMMA) {
+                BmRec r{p.bm, p.T, t, seg_start(p, t)};
+                r.put(r.start);  // phase 0 starts a sample at the segment start
+                while (s.pos < end) {
+                    d.sample(s, tl);
+                    c++;
+                    r.put(s.pos);
+                }
+                r.close();
+            } else {
+                while (s.pos < end) {
+                    d.sample(s, tl);
+                    c++;
+                }
             }
+        }
         if (d.paired()) {
             typename SrcOf<E, D>::type s1;
             make_src<E>(p, t, seg_start(p, t), s1);
             d.skip_second(s1, tl);
             u64 c1 = 0;
+            BmRec r{p.bm ? p.bm + (size_t)BM_WORDS * p.T : nullptr, p.T, t, seg_start(p, t)};
+            r.put(s1.pos);  // phase 1's first full sample starts after the lone second
             while (s1.pos < end) {
                 d.sample(s1, tl);
                 c1++;
+                r.put(s1.pos);
             }
+            r.close();
             cnt1[t] = c1;
             ex1[t] = (u32)(s1.pos - end);
         }
@@ -494,6 +542,46 @@ template <int E, int D>
 __device__ void resolve_entry(const FillPlan &p, const ZigFast *sm, u32 t, u32 e, u64 c0, u32 x0, u64 c1, u32 x1,
                               u64 &cnt, u32 &ex) {
     const u64 start = seg_start(p, t), end = seg_end(p, t);
+    if constexpr (D == FAM_GAMMA) {
+        if (p.bm) {  // B alone, meeting points looked up in the count pass's bitmaps
+            typename SrcOf<E, D>::type sb;
+            make_src<E>(p, t, start + e, sb);
+            typename DistOf<D>::type d;
+            make_dist<D>(p, sm, d);
+            Tally tl;
+            const bool two = d.paired();
+            const u32 *bm0 = p.bm, *bm1 = p.bm + (size_t)BM_WORDS * p.T;
+            u64 nb = 0;
+            u32 kw = ~0u, wa = 0, wc = 0;
+            while (true) {
+                if (sb.pos >= end) {
+                    cnt = nb;
+                    ex = (u32)(sb.pos - end);
+                    return;
+                }
+                u64 q = sb.pos - start;
+                if (q >= BM_UNITS) break;
+                u32 k = (u32)(q >> 5), bit = 1u << (q & 31);
+                if (k != kw) {
+                    kw = k;
+                    wa = bm0[(size_t)k * p.T + t];
+                    if (two) wc = bm1[(size_t)k * p.T + t];
+                }
+                if (wa & bit) {
+                    cnt = c0 - bm_rank(bm0, p.T, t, q) + nb;
+                    ex = x0;
+                    return;
+                }
+                if (two && (wc & bit)) {
+                    cnt = c1 - bm_rank(bm1, p.T, t, q) + nb;
+                    ex = x1;
+                    return;
+                }
+                d.sample(sb, tl);
+                nb++;
+            }
+        }  // no meeting in the recorded window: the lockstep parse below
+    }
     typename SrcOf<E, D>::type sa, sb, sc;
     make_src<E>(p, t, start, sa);
     make_src<E>(p, t, start + e, sb);
@@ -1134,6 +1222,7 @@ struct DevCtx {
     size_t cap_T = 0;
     u64 *states = nullptr, *cnt0 = nullptr, *cnt1 = nullptr, *cnt = nullptr, *off = nullptr;
     u32 *ex0 = nullptr, *ex1 = nullptr, *exA = nullptr, *exB = nullptr, *entry = nullptr;
+    u32 *bm = nullptr;  // [2][BM_WORDS][T] boundary bitmaps
     void *cub_tmp = nullptr;
     size_t cub_bytes = 0;
     DevResult *res = nullptr;
@@ -1194,6 +1283,7 @@ rs_status ensure_scratch(DevCtx &c, size_t T) {
     size_t nT = T + T / 4;
     cudaFree(c.states); cudaFree(c.cnt0); cudaFree(c.cnt1); cudaFree(c.cnt); cudaFree(c.off);
     cudaFree(c.ex0); cudaFree(c.ex1); cudaFree(c.exA); cudaFree(c.exB); cudaFree(c.entry); cudaFree(c.cub_tmp);
+    cudaFree(c.bm);
     CK(cudaMalloc(&c.states, nT * 32));
     CK(cudaMalloc(&c.cnt0, nT * 8));
     CK(cudaMalloc(&c.cnt1, nT * 8));
@@ -1204,6 +1294,7 @@ rs_status ensure_scratch(DevCtx &c, size_t T) {
     CK(cudaMalloc(&c.exA, nT * 4));
     CK(cudaMalloc(&c.exB, nT * 4));
     CK(cudaMalloc(&c.entry, nT * 4));
+    CK(cudaMalloc(&c.bm, nT * 4 * 2 * BM_WORDS));
     c.cub_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, c.cub_bytes, c.cnt, c.off, (int)nT);
     CK(cudaMalloc(&c.cub_tmp, c.cub_bytes));
@@ -1882,6 +1973,7 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
             p.words = c.words;
             p.nwords = nw;
         }
+        p.bm = r.family == FAM_GAMMA ? c.bm : nullptr;  // read now: the steps above may grow the scratch
         CK(cudaMemsetAsync(c.res, 0, offsetof(DevResult, serial_state), st));
         unsigned g = p.T / BLOCK;
         int round = 0;
