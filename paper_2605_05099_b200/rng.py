@@ -38,6 +38,8 @@ _STREAM_METHODS = {  # rng.py:27-35
 }
 
 # the reference's continuous + discrete names (continuous.py:339-359, discrete.py:95-100)
+RAW_DEVICE_WORDS = 4096  # raw(nbytes) from this many words on goes through the device uint64 fill
+
 SCALAR_NAMES = ("u01", "u01f", "unif", "uniff", "norm", "normf", "exp", "expf", "lognormal", "gamma", "beta",
                 "chi2", "t", "f", "gumbel", "pareto", "gpd", "weibull", "skew_normal")
 DISCRETE_NAMES = ("uint8", "uint16", "uint32", "uint64", "int", "long_long")
@@ -130,10 +132,18 @@ class Rng:
 
     @_op
     def raw(self, nbytes):
-        """rng.py:80-94: little-endian bytes; a trailing partial word is truncated."""
+        """rng.py:80-94: little-endian bytes; a trailing partial word is truncated.
+
+        The byte pipe is ceil(nbytes / 8) u64 takes, i.e. a raw uint64 fill: from
+        RAW_DEVICE_WORDS words on it runs on the device (same words, same position)."""
         nbytes = int(nbytes)
         if nbytes < 0:
             raise ValueError("byte count must be >= 0")
+        words = (nbytes + 7) // 8
+        if words >= RAW_DEVICE_WORDS:
+            host = np.empty(words, dtype="<u8")
+            self.device_fill("uint64", [], [0, 0], words, out=host)
+            return host.view(np.uint8)[:nbytes].tobytes()
         full, rest = divmod(nbytes, 8)
         out = bytearray()
         for _ in range(full):

@@ -380,3 +380,20 @@ def test_c5b_full_2p28(m):
     for j in rows:
         o = O.OracleRng("sfc64", seed=[31], spawn_key=(int(j),))
         assert np.array_equal(host[j], o.fill("uint64", {"b": m}, (1 << 28) // S)), j
+
+
+@pytest.mark.parametrize("engine", ["x256**", "philox", "pcg64", "x256++simd"])
+def test_raw_bytes_device(engine):
+    """raw(nbytes) (rng.py:80-94) past RAW_DEVICE_WORDS: the device uint64 fill gives the
+    same bytes and leaves the same position as the oracle's u64 takes, after a pending half."""
+    from paper_2605_05099_b200.rng import RAW_DEVICE_WORDS
+    words = RAW_DEVICE_WORDS + 777
+    nbytes = 8 * words - 3
+    r = state_io.create(engine, seed=[5])
+    o = O.OracleRng(engine, seed=[5])
+    assert r.next_u32() == o.next_u32()
+    got = r.raw(nbytes)
+    ref = np.ascontiguousarray(o.fill("uint64", {}, words), dtype="<u8").view(np.uint8)[:nbytes].tobytes()
+    assert got == ref
+    _assert_same_position(r, o)
+    assert r.next_u64() == o.next_u64()
