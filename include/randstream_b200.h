@@ -16,7 +16,7 @@
  *   rs_mvn           replaces Rng.mvn(mean, cov, n, layout)  rng.py:273-275,
  *                    continuous.py:312-336 (the factor L is computed by the caller)
  *   rs_engine_*      the engine protocol used for stream positioning and the
- *                    144-word buffer refills: generate (engines/*.py generate),
+ *                    144-word buffer refills: generate (engines/<name>.py generate),
  *                    seed (seeding.py:115-116 + engines seed_from), jump/advance
  *                    (rng.py:135-171, jumps.py:116-126, pcg.py:41-55, ranlux.py:90-93)
  *   rs_last_error    replaces the per-handle error slot (rng.py:38-52, state_io.py:45-47)

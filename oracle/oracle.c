@@ -34,7 +34,7 @@ typedef unsigned __int128 u128;
 #define M64 0xFFFFFFFFFFFFFFFFULL
 
 /* engine ids follow the reference registry order, src/engines/__init__.py:11-26 */
-enum { E_X256PP = 1, E_X256SS = 2, E_PCG64 = 5, E_PHILOX = 6, E_SFC64 = 8, E_RANLUX = 10,
+enum { E_X256PP = 1, E_X256SS = 2, E_PCG64 = 5, E_PHILOX = 6, E_SFC64 = 8, E_RANLUX = 10, E_X128P = 3, E_XORO = 4, E_SQUARES = 7, E_CWG128 = 9, E_CHACHA20 = 11,
        E_X256PP_SIMD = 12, E_X256SS_SIMD = 13, E_SFC64_SIMD = 14 };
 
 /* distribution ids, shared with include/randstream_b200.h */
@@ -137,6 +137,83 @@ static void gen_sfc(uint64_t *s, uint64_t *out, int n) {
     s[0] = a; s[1] = b; s[2] = c; s[3] = w;
 }
 
+/* xorshift128+, src/engines/xorfam.py:127-146 (state a, b; word a + b) */
+static void gen_x128p(uint64_t *s, uint64_t *out, int n) {
+    for (int i = 0; i < n; i++) {
+        uint64_t s1 = s[0], s0 = s[1];
+        out[i] = s0 + s1;
+        s1 ^= s1 << 23;
+        s[0] = s0;
+        s[1] = s1 ^ s0 ^ (s1 >> 18) ^ (s0 >> 5);
+    }
+}
+/* xoroshiro128++, src/engines/xorfam.py:149-168 */
+static void gen_xoro(uint64_t *s, uint64_t *out, int n) {
+    for (int i = 0; i < n; i++) {
+        uint64_t s0 = s[0], s1 = s[1];
+        out[i] = rotl(s0 + s1, 17) + s0;
+        s1 ^= s0;
+        s[0] = rotl(s0, 49) ^ s1 ^ (s1 << 21);
+        s[1] = rotl(s1, 28);
+    }
+}
+/* squares64, src/engines/counter.py:27-45 (state counter, key) */
+static uint64_t sq_rot32(uint64_t x) { return (x >> 32) | (x << 32); }
+static void gen_squares(uint64_t *s, uint64_t *out, int n) {
+    for (int i = 0; i < n; i++) {
+        uint64_t key = s[1], y = s[0] * key, x = y, z = y + key;
+        x = x * x + y; x = sq_rot32(x);
+        x = x * x + z; x = sq_rot32(x);
+        x = x * x + y; x = sq_rot32(x);
+        x = x * x + z;
+        uint64_t t = x;
+        x = sq_rot32(x);
+        out[i] = t ^ ((x * x + y) >> 32);
+        s[0] += 1;
+    }
+}
+/* ChaCha20 keystream, src/engines/counter.py:170-216 (state: key[4], nonce0|nonce1<<32,
+ * nonce2|counter<<32); the caller keeps the 32-bit counter in range */
+static uint32_t rl32(uint32_t x, int r) { return (x << r) | (x >> (32 - r)); }
+static void gen_chacha(uint64_t *s, uint64_t *out, int n) {
+    static const int q[8][4] = {{0, 4, 8, 12}, {1, 5, 9, 13}, {2, 6, 10, 14}, {3, 7, 11, 15},
+                                {0, 5, 10, 15}, {1, 6, 11, 12}, {2, 7, 8, 13}, {3, 4, 9, 14}};
+    for (int b = 0; b < n / 8; b++) {
+        uint32_t in[16], x[16];
+        in[0] = 0x61707865u; in[1] = 0x3320646Eu; in[2] = 0x79622D32u; in[3] = 0x6B206574u;
+        for (int i = 0; i < 4; i++) { in[4 + 2 * i] = (uint32_t)s[i]; in[5 + 2 * i] = (uint32_t)(s[i] >> 32); }
+        in[12] = (uint32_t)(s[5] >> 32);
+        in[13] = (uint32_t)s[4]; in[14] = (uint32_t)(s[4] >> 32); in[15] = (uint32_t)s[5];
+        memcpy(x, in, sizeof x);
+        for (int dr = 0; dr < 10; dr++)
+            for (int k = 0; k < 8; k++) {
+                int a = q[k][0], bb = q[k][1], c = q[k][2], d = q[k][3];
+                x[a] += x[bb]; x[d] = rl32(x[d] ^ x[a], 16);
+                x[c] += x[d]; x[bb] = rl32(x[bb] ^ x[c], 12);
+                x[a] += x[bb]; x[d] = rl32(x[d] ^ x[a], 8);
+                x[c] += x[d]; x[bb] = rl32(x[bb] ^ x[c], 7);
+            }
+        for (int i = 0; i < 8; i++)
+            out[8 * b + i] = (uint64_t)(uint32_t)(x[2 * i] + in[2 * i]) |
+                             ((uint64_t)(uint32_t)(x[2 * i + 1] + in[2 * i + 1]) << 32);
+        s[5] = (s[5] & 0xFFFFFFFFULL) | ((uint64_t)(uint32_t)(in[12] + 1) << 32);
+    }
+}
+/* cwg128, src/engines/cwg.py:28-36 (x, weyl, extra, inc as lo/hi word pairs) */
+static void gen_cwg(uint64_t *s, uint64_t *out, int n) {
+    typedef unsigned __int128 w128;
+    w128 x = ((w128)s[1] << 64) | s[0], weyl = ((w128)s[3] << 64) | s[2];
+    w128 extra = ((w128)s[5] << 64) | s[4], inc = ((w128)s[7] << 64) | s[6];
+    for (int i = 0; i < n; i++) {
+        weyl += x;
+        extra += inc;
+        x = ((x >> 1) * (weyl | 1)) ^ extra;
+        out[i] = (uint64_t)(weyl >> 96) ^ (uint64_t)x;
+    }
+    s[0] = (uint64_t)x; s[1] = (uint64_t)(x >> 64); s[2] = (uint64_t)weyl; s[3] = (uint64_t)(weyl >> 64);
+    s[4] = (uint64_t)extra; s[5] = (uint64_t)(extra >> 64);
+}
+
 /* ranlux++: 576-bit residue times A mod m = 2^576 - 2^240 + 1,
  * src/engines/ranlux.py:16-61.  Any exact reduction gives the same residue. */
 static const uint64_t RLX_M[9] = {1, 0, 0, 0xFFFF000000000000ULL, M64, M64, M64, M64, M64};
@@ -235,14 +312,24 @@ static void gen_ranlux(uint64_t *s, uint64_t *out, int n) {
 
 static int engine_state_words(int eid) {
     switch (eid) {
-    case E_PHILOX: return 6;
+    case E_PHILOX: case E_CHACHA20: return 6;
     case E_RANLUX: return 9;
+    case E_X128P: case E_XORO: case E_SQUARES: return 2;
+    case E_CWG128: return 8;
     case E_X256PP_SIMD: case E_X256SS_SIMD: case E_SFC64_SIMD: return 32;
     default: return 4;
     }
 }
 static int engine_seed_words(int eid) {
-    switch (eid) { case E_PHILOX: return 2; case E_SFC64: case E_SFC64_SIMD: return 3; case E_RANLUX: return 9; default: return 4; }
+    switch (eid) {
+    case E_PHILOX: case E_X128P: case E_XORO: return 2;
+    case E_SQUARES: return 1;
+    case E_SFC64: case E_SFC64_SIMD: return 3;
+    case E_CHACHA20: return 6;
+    case E_CWG128: return 8;
+    case E_RANLUX: return 9;
+    default: return 4;
+    }
 }
 
 /* 8-lane interleaved engines, src/engines/interleave.py:71-76: word i from lane i mod 8 */
@@ -265,6 +352,11 @@ static void engine_generate(int eid, uint64_t *s, uint64_t *out, int n) {
     case E_PHILOX: gen_philox(s, out, n); break;
     case E_SFC64: gen_sfc(s, out, n); break;
     case E_RANLUX: rlx_init(); gen_ranlux(s, out, n); break;
+    case E_X128P: gen_x128p(s, out, n); break;
+    case E_XORO: gen_xoro(s, out, n); break;
+    case E_SQUARES: gen_squares(s, out, n); break;
+    case E_CHACHA20: gen_chacha(s, out, n); break;
+    case E_CWG128: gen_cwg(s, out, n); break;
     }
 }
 
@@ -338,6 +430,13 @@ static void engine_seed_from(int eid, uint64_t *s, const uint64_t *w) {
         if (!(s[0] | s[1] | s[2] | s[3])) s[0] = 1;
         break;
     case E_PCG64: s[0] = w[0]; s[1] = w[1]; s[2] = w[2] | 1; s[3] = w[3]; break;
+    case E_X128P: case E_XORO:  /* xorfam.py:66-70 */
+        s[0] = w[0]; s[1] = w[1];
+        if (!(s[0] | s[1])) s[0] = 1;
+        break;
+    case E_SQUARES: s[0] = 0; s[1] = w[0]; break;                         /* counter.py:63-65 */
+    case E_CHACHA20: memcpy(s, w, 40); s[5] = w[5] & 0xFFFFFFFFULL; break;  /* counter.py:228-233 */
+    case E_CWG128: memcpy(s, w, 64); s[6] |= 1; break;                     /* cwg.py:62-67 */
     case E_PHILOX: s[0] = s[1] = s[2] = s[3] = 0; s[4] = w[0]; s[5] = w[1]; break;
     case E_SFC64: s[0] = w[0]; s[1] = w[1]; s[2] = w[2]; s[3] = 1; break;
     case E_RANLUX: {
@@ -873,6 +972,33 @@ void orc_ranlux_advance_chunks(uint64_t *s, uint64_t nlo, uint64_t nhi) {
 }
 void orc_ranlux_mulmod(const uint64_t *x, const uint64_t *y, uint64_t *out) { rlx_init(); rlx_mulmod(x, y, out); }
 void orc_engine_generate(int eid, uint64_t *s, uint64_t *out, int n) { engine_generate(eid, s, out, n); }
+
+/* 2^k steps of xorshift128+ / xoroshiro128 (src/jumps.py: T^N = (x^N mod p)(T), so the
+ * same map as the matrix T^(2^k)); T by unit vectors, then k squarings */
+typedef struct { uint64_t c[128][2]; } m128;
+static void m128_vec(const m128 *m, const uint64_t v[2], uint64_t o[2]) {
+    uint64_t a = 0, b = 0;
+    for (int j = 0; j < 128; j++)
+        if ((v[j >> 6] >> (j & 63)) & 1) { a ^= m->c[j][0]; b ^= m->c[j][1]; }
+    o[0] = a; o[1] = b;
+}
+void orc_x128_jump_pow2k(int eid, uint64_t *s, int k) {
+    static m128 t, sq;
+    for (int j = 0; j < 128; j++) {
+        uint64_t v[2] = {0, 0}, w[2];
+        v[j >> 6] = 1ULL << (j & 63);
+        uint64_t tmp[2] = {v[0], v[1]};
+        if (eid == E_X128P) gen_x128p(tmp, w, 1); else gen_xoro(tmp, w, 1);
+        t.c[j][0] = tmp[0]; t.c[j][1] = tmp[1];
+    }
+    for (int i = 0; i < k; i++) {
+        for (int j = 0; j < 128; j++) m128_vec(&t, t.c[j], sq.c[j]);
+        t = sq;
+    }
+    uint64_t o[2];
+    m128_vec(&t, s, o);
+    s[0] = o[0]; s[1] = o[1];
+}
 
 /* ---------------------------------------------------------------- threaded CPU baseline */
 /* The --impl reference / cpu_baseline leg: P host threads, each running this

@@ -22,9 +22,10 @@ import numpy as np
 HERE = pathlib.Path(__file__).resolve().parent
 LIB_PATH = HERE / "liboracle.so"
 
-ENGINE_IDS = {"x256++": 1, "x256**": 2, "pcg64": 5, "philox": 6, "sfc64": 8, "ranlux++": 10,
-              "x256++simd": 12, "x256**simd": 13, "sfc64simd": 14}
-STATE_WORDS = {1: 4, 2: 4, 5: 4, 6: 6, 8: 4, 10: 9, 12: 32, 13: 32, 14: 32}
+ENGINE_IDS = {"x256++": 1, "x256**": 2, "x128+": 3, "xoro++": 4, "pcg64": 5, "philox": 6, "squares": 7,
+              "sfc64": 8, "cwg128": 9, "ranlux++": 10, "chacha20": 11, "x256++simd": 12, "x256**simd": 13,
+              "sfc64simd": 14}
+STATE_WORDS = {1: 4, 2: 4, 3: 2, 4: 2, 5: 4, 6: 6, 7: 2, 8: 4, 9: 8, 10: 9, 11: 6, 12: 32, 13: 32, 14: 32}
 DIST_IDS = {"uint64": 1, "u01": 2, "u01f": 3, "norm": 4, "exp": 5, "gamma": 6, "beta": 7, "stdnorm": 8,
             "unif": 9, "uniff": 10, "normf": 11, "expf": 12, "lognormal": 13, "chi2": 14, "t": 15, "f": 16,
             "gumbel": 17, "pareto": 18, "gpd": 19, "weibull": 20, "skew_normal": 21,
@@ -88,6 +89,7 @@ def lib():
         L.orc_pcg_advance.argtypes = [U64P, ctypes.c_uint64, ctypes.c_uint64]
         L.orc_ranlux_advance_chunks.argtypes = [U64P, ctypes.c_uint64, ctypes.c_uint64]
         L.orc_ranlux_jump_pow2k.argtypes = [U64P, ctypes.c_int]
+        L.orc_x128_jump_pow2k.argtypes = [ctypes.c_int, U64P, ctypes.c_int]
         L.orc_engine_generate.argtypes = [ctypes.c_int, U64P, U64P, ctypes.c_int]
         _LIB = L
     return _LIB
@@ -279,6 +281,13 @@ def ranlux_advance_chunks(state, nchunks):
     s, _ = _u64arr(state)
     lib().orc_ranlux_advance_chunks(s, nchunks & 0xFFFFFFFFFFFFFFFF, nchunks >> 64)
     return [int(s[i]) for i in range(9)]
+
+
+def x128_jump(engine, state, k):
+    """2^k steps of x128+ / xoro++ (jumps.py FAMILY_JUMPS)."""
+    s, _ = _u64arr(state)
+    lib().orc_x128_jump_pow2k(ENGINE_IDS[engine], s, int(k))
+    return [int(s[i]) for i in range(2)]
 
 
 def ranlux_jump(state, k):

@@ -111,6 +111,8 @@ def check(status):
         return
     msg = last_error() or "status %d" % status
     if status == RS_ERR_VALUE:
+        if "stream exhausted" in msg:  # chacha20's 32-bit block counter, counter.py:212-213
+            raise OverflowError("stream exhausted")
         raise ValueError(msg)
     if status == RS_ERR_UNSUPPORTED:
         raise NotImplementedError(msg)

@@ -179,6 +179,98 @@ struct EngSfc {  // sfc.py:25-36
     }
 };
 
+// xorshift128+ (xorfam.py:127-146): state [a, b], word a + b
+struct EngX128p {
+    u64 a, b;
+    RS_DEV void load(const u64 *p) { a = p[0]; b = p[1]; }
+    RS_DEV u64 next() {
+        u64 r = a + b, s1 = a, s0 = b;
+        s1 ^= s1 << 23;
+        a = s0;
+        b = s1 ^ s0 ^ (s1 >> 18) ^ (s0 >> 5);
+        return r;
+    }
+};
+// xoroshiro128++ (xorfam.py:149-168)
+struct EngXoro {
+    u64 s0, s1;
+    RS_DEV void load(const u64 *p) { s0 = p[0]; s1 = p[1]; }
+    RS_DEV u64 next() {
+        u64 r = rotl64(s0 + s1, 17) + s0, t = s1 ^ s0;
+        s0 = rotl64(s0, 49) ^ t ^ (t << 21);
+        s1 = rotl64(t, 28);
+        return r;
+    }
+};
+// squares64 (counter.py:12-48): word i = f(counter + i, key)
+RS_DEV u64 sq_swap(u64 x) { return (x >> 32) | (x << 32); }
+struct EngSquares {
+    u64 ctr, key;
+    RS_DEV u64 next() {
+        u64 x = ctr++ * key, y = x, z = y + key;
+        x = sq_swap(x * x + y);
+        x = sq_swap(x * x + z);
+        x = sq_swap(x * x + y);
+        u64 t = x = x * x + z;
+        x = sq_swap(x);
+        return t ^ ((x * x + y) >> 32);
+    }
+};
+// ChaCha20 (counter.py:144-216): 64-byte blocks of the 32-bit block counter, served as
+// eight little-endian words
+RS_DEV u32 rotl32d(u32 x, int r) { return __funnelshift_l(x, x, r); }
+#define RS_CHACHA_QR(a, b, c, d)                                   \
+    a += b; d = rotl32d(d ^ a, 16); c += d; b = rotl32d(b ^ c, 12); \
+    a += b; d = rotl32d(d ^ a, 8); c += d; b = rotl32d(b ^ c, 7);
+struct EngChacha {
+    u32 k[8], n0, n1, n2, ctr;
+    u64 o[8];
+    int left;
+    RS_DEV void block() {
+        const u32 c0 = 0x61707865u, c1 = 0x3320646Eu, c2 = 0x79622D32u, c3 = 0x6B206574u;
+        u32 x0 = c0, x1 = c1, x2 = c2, x3 = c3, x4 = k[0], x5 = k[1], x6 = k[2], x7 = k[3];
+        u32 x8 = k[4], x9 = k[5], x10 = k[6], x11 = k[7], x12 = ctr, x13 = n0, x14 = n1, x15 = n2;
+#pragma unroll 2
+        for (int r = 0; r < 10; r++) {
+            RS_CHACHA_QR(x0, x4, x8, x12) RS_CHACHA_QR(x1, x5, x9, x13)
+            RS_CHACHA_QR(x2, x6, x10, x14) RS_CHACHA_QR(x3, x7, x11, x15)
+            RS_CHACHA_QR(x0, x5, x10, x15) RS_CHACHA_QR(x1, x6, x11, x12)
+            RS_CHACHA_QR(x2, x7, x8, x13) RS_CHACHA_QR(x3, x4, x9, x14)
+        }
+        o[0] = (u64)(x0 + c0) | ((u64)(x1 + c1) << 32);
+        o[1] = (u64)(x2 + c2) | ((u64)(x3 + c3) << 32);
+        o[2] = (u64)(x4 + k[0]) | ((u64)(x5 + k[1]) << 32);
+        o[3] = (u64)(x6 + k[2]) | ((u64)(x7 + k[3]) << 32);
+        o[4] = (u64)(x8 + k[4]) | ((u64)(x9 + k[5]) << 32);
+        o[5] = (u64)(x10 + k[6]) | ((u64)(x11 + k[7]) << 32);
+        o[6] = (u64)(x12 + ctr) | ((u64)(x13 + n0) << 32);
+        o[7] = (u64)(x14 + n1) | ((u64)(x15 + n2) << 32);
+        ctr++;
+    }
+    RS_DEV u64 next() {
+        if (left == 0) {
+            block();
+            left = 8;
+        }
+        u64 r = o[0];
+#pragma unroll
+        for (int i = 0; i < 7; i++) o[i] = o[i + 1];
+        left--;
+        return r;
+    }
+};
+#undef RS_CHACHA_QR
+// cwg128 (cwg.py:28-36): 128-bit x, Weyl state, additive state, odd increment
+struct EngCwg {
+    unsigned __int128 x, weyl, extra, inc;
+    RS_DEV u64 next() {
+        weyl += x;
+        extra += inc;
+        x = ((x >> 1) * (weyl | 1)) ^ extra;
+        return (u64)(weyl >> 96) ^ (u64)x;
+    }
+};
+
 // sfc64simd (interleave.py:172-187): 8 sfc64 lanes, word i from lane i mod 8
 struct EngSfcSimd {
     EngSfc l[8];

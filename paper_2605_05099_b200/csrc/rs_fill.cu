@@ -31,6 +31,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -121,6 +122,11 @@ template <> struct EngOf<RS_ENG_PHILOX> { typedef EngPhilox type; };
 template <> struct EngOf<RS_ENG_RANLUX> { typedef EngRanlux type; };
 template <> struct EngOf<RS_ENG_SFC64> { typedef EngSfc type; };
 template <> struct EngOf<RS_ENG_SFC64_SIMD> { typedef EngSfcSimd type; };
+template <> struct EngOf<RS_ENG_X128P> { typedef EngX128p type; };
+template <> struct EngOf<RS_ENG_XORO> { typedef EngXoro type; };
+template <> struct EngOf<RS_ENG_SQUARES> { typedef EngSquares type; };
+template <> struct EngOf<RS_ENG_CHACHA20> { typedef EngChacha type; };
+template <> struct EngOf<RS_ENG_CWG128> { typedef EngCwg type; };
 
 // Parse source for engines whose words are expensive (Philox-4x64, ranlux++): the
 // chunk's engine words are materialized once by the coalesced fixed-fill kernel and
@@ -153,8 +159,25 @@ template <> struct EngOf<RS_ENG_MEM> { typedef EngMem type; };
 // engine positioned at engine word t*L of the chunk (thread t's segment start)
 template <int E>
 __device__ __forceinline__ void make_engine(const FillPlan &p, u32 t, typename EngOf<E>::type &e) {
-    if constexpr (E == RS_ENG_X256SS || E == RS_ENG_X256PP) {
-        e.load(p.x256_states + 4 * (u64)t);
+    if constexpr (E == RS_ENG_X256SS || E == RS_ENG_X256PP || E == RS_ENG_X128P || E == RS_ENG_XORO) {
+        e.load(p.x256_states + 4 * (u64)t);  // 128-bit engines use words 0, 1 of the padded state
+    } else if constexpr (E == RS_ENG_SQUARES) {
+        e.ctr = p.base[0] + (u64)t * p.L;
+        e.key = p.base[1];
+    } else if constexpr (E == RS_ENG_CHACHA20) {
+#pragma unroll
+        for (int i = 0; i < 4; i++) { e.k[2 * i] = (u32)p.base[i]; e.k[2 * i + 1] = (u32)(p.base[i] >> 32); }
+        e.n0 = (u32)p.base[4];
+        e.n1 = (u32)(p.base[4] >> 32);
+        e.n2 = (u32)p.base[5];
+        e.ctr = (u32)(p.base[5] >> 32) + (u32)((u64)t * (p.L / 8));  // the host checked 2^32
+        e.left = 0;
+    } else if constexpr (E == RS_ENG_CWG128) {
+        typedef unsigned __int128 U;
+        e.x = ((U)p.base[1] << 64) | p.base[0];
+        e.weyl = ((U)p.base[3] << 64) | p.base[2];
+        e.extra = ((U)p.base[5] << 64) | p.base[4];
+        e.inc = ((U)p.base[7] << 64) | p.base[6];
     } else if constexpr (E == RS_ENG_PCG64) {
         e.slo = p.base[0]; e.shi = p.base[1]; e.ilo = p.base[2]; e.ihi = p.base[3];
         for (int j = 0; j < MAXLEV && (t >> j); j++)
@@ -261,7 +284,7 @@ __device__ __forceinline__ void make_src(const FillPlan &p, u32 t, u64 hpos, HSr
 
 // ---- sampler families (template key) and their construction from the plan
 enum { FAM_LEMIRE = RS_DIST_UINT64, FAM_NORM = RS_DIST_NORM, FAM_EXP = RS_DIST_EXP, FAM_GAMMA = RS_DIST_GAMMA,
-       FAM_F32 = 11, FAM_U32 = 22 };
+       FAM_F32 = 11, FAM_U32 = 22, FAM_FIXED = 40 /* per-stream mode: a fixed map of each word */ };
 template <int D> struct DistOf;
 template <> struct DistOf<FAM_NORM> { typedef DistNorm type; };
 template <> struct DistOf<FAM_EXP> { typedef DistExp type; };
@@ -720,7 +743,9 @@ enum { WK_UNIF = 0, WK_GUMBEL = 1, WK_I64 = 2 };                  // FX_WMAP kin
 enum { HK_UNIFF = 0, HK_MASK = 1, HK_POW2 = 2, HK_I32 = 3 };       // FX_HMAP kinds
 constexpr bool is_half(int mode) { return mode == FX_U01F || mode == FX_HMAP; }
 
-__device__ __forceinline__ u32 hmap(const FillPlan &p, u32 h) {
+// PL = FillPlan or StreamArgs (both carry fp, ip, fm, kind)
+template <class PL>
+__device__ __forceinline__ u32 hmap(const PL &p, u32 h) {
     switch (p.kind) {
     case HK_UNIFF:  // _f32(a + u01f * (b - a)), continuous.py:143-147
         return __float_as_uint(__double2float_rn(p.fp[0] + (double)u01f_of(h, p.fm) * (p.fp[1] - p.fp[0])));
@@ -730,8 +755,8 @@ __device__ __forceinline__ u32 hmap(const FillPlan &p, u32 h) {
     }
 }
 
-template <int MODE>
-__device__ __forceinline__ u64 fx_map(const FillPlan &p, u64 w) {
+template <int MODE, class PL>
+__device__ __forceinline__ u64 fx_map(const PL &p, u64 w) {
     if constexpr (MODE == FX_RAW) return w;
     else if constexpr (MODE == FX_POW2) return __umul64hi(w, p.ip[0]);
     else if constexpr (MODE == FX_U01) return bits(u01_of(w, p.fm));
@@ -992,7 +1017,8 @@ struct SerialHSrc {
     }
 };
 
-__device__ u64 fx_map_rt(const FillPlan &p, u64 w) {
+template <class PL>
+__device__ u64 fx_map_rt(const PL &p, u64 w) {
     switch (p.fmode) {
     case FX_RAW: return fx_map<FX_RAW>(p, w);
     case FX_POW2: return fx_map<FX_POW2>(p, w);
@@ -1060,6 +1086,11 @@ __global__ void k_serial(const __grid_constant__ FillPlan p, DevResult *res) {
             res->serial_state[4 * k] = f.l[k].a; res->serial_state[4 * k + 1] = f.l[k].b;
             res->serial_state[4 * k + 2] = f.l[k].c; res->serial_state[4 * k + 3] = f.l[k].w;
         }
+    } else if constexpr (E == RS_ENG_CWG128) {
+        res->serial_state[0] = (u64)f.x; res->serial_state[1] = (u64)(f.x >> 64);
+        res->serial_state[2] = (u64)f.weyl; res->serial_state[3] = (u64)(f.weyl >> 64);
+        res->serial_state[4] = (u64)f.extra; res->serial_state[5] = (u64)(f.extra >> 64);
+        res->serial_state[6] = (u64)f.inc; res->serial_state[7] = (u64)(f.inc >> 64);
     } else {
         res->serial_state[0] = f.a; res->serial_state[1] = f.b;
         res->serial_state[2] = f.c; res->serial_state[3] = f.w;
@@ -1070,7 +1101,7 @@ __global__ void k_serial(const __grid_constant__ FillPlan p, DevResult *res) {
 // SeedSequenceFE128 on the device (seeding.py:48-116): stream j's state from
 // entropy (ip words in `seedw`) + spawn key prefix + (j0 + j).
 struct StreamArgs {
-    int engine, nseed, nprefix, dist, fm;
+    int engine, nseed, nprefix, dist, fm, fmode;
     u64 seed[16];
     u64 prefix[8];
     u64 j0, nstreams, nper;
@@ -1156,19 +1187,62 @@ __global__ void __launch_bounds__(BLOCK) k_streams(const __grid_constant__ Strea
     } else if constexpr (E == RS_ENG_PHILOX) {
         seed_fe128(a, a.j0 + j, w, 2);
         e.c0 = e.c1 = e.c2 = e.c3 = 0; e.k0 = w[0]; e.k1 = w[1]; e.left = 0;
+    } else if constexpr (E == RS_ENG_X128P || E == RS_ENG_XORO) {  // xorfam.py:66-70
+        seed_fe128(a, a.j0 + j, w, 2);
+        if (!(w[0] | w[1])) w[0] = 1;
+        e.load(w);
+    } else if constexpr (E == RS_ENG_SQUARES) {  // counter.py:63-65
+        seed_fe128(a, a.j0 + j, w, 1);
+        e.ctr = 0;
+        e.key = w[0];
+    } else if constexpr (E == RS_ENG_CHACHA20) {  // counter.py:228-233
+        seed_fe128(a, a.j0 + j, w, 6);
+#pragma unroll
+        for (int i = 0; i < 4; i++) { e.k[2 * i] = (u32)w[i]; e.k[2 * i + 1] = (u32)(w[i] >> 32); }
+        e.n0 = (u32)w[4]; e.n1 = (u32)(w[4] >> 32); e.n2 = (u32)w[5];
+        e.ctr = 0;
+        e.left = 0;
+    } else if constexpr (E == RS_ENG_CWG128) {  // cwg.py:62-67
+        seed_fe128(a, a.j0 + j, w, 8);
+        typedef unsigned __int128 U;
+        e.x = ((U)w[1] << 64) | w[0];
+        e.weyl = ((U)w[3] << 64) | w[2];
+        e.extra = ((U)w[5] << 64) | w[4];
+        e.inc = (((U)w[7] << 64) | w[6]) | 1;
     } else {  // x256
         seed_fe128(a, a.j0 + j, w, 4);
         if (!(w[0] | w[1] | w[2] | w[3])) w[0] = 1;
         e.s0 = w[0]; e.s1 = w[1]; e.s2 = w[2]; e.s3 = w[3];
     }
-    typedef typename DistOf<D>::type DT;
+    // Per-stream rows go out through VecWriter8 (8-byte) / ScalarWriter (4-byte). The
+    // shared-memory RingWriter used by k_emit produced an illegal address here in some
+    // configurations (x256**/pcg64 normals, >= 8 streams) that vanished under printf
+    // instrumentation; it stays out of this kernel until that is understood.
+    if constexpr (D == FAM_FIXED) {  // raw / uniform / masked laws: a fresh stream, no pending half
+        if (is_half(a.fmode)) {  // low half first, a trailing high half dropped
+            ScalarWriter<u32> wr;
+            wr.init((u32 *)a.out, j * a.nper);
+            for (u64 i = 0; i < a.nper; i += 2) {
+                u64 q = fx_map_rt(a, e.next());
+                wr.put((u32)q);
+                if (i + 1 < a.nper) wr.put((u32)(q >> 32));
+            }
+            wr.finish();
+        } else {
+            VecWriter8<u64> wr;
+            wr.init((u64 *)a.out, j * a.nper);
+            for (u64 i = 0; i < a.nper; i++) wr.put(fx_map_rt(a, e.next()));
+            wr.finish();
+        }
+        return;
+    }
+    typedef typename DistOf<D == FAM_FIXED ? FAM_LEMIRE : D>::type DT;
     DT d;
     DistArgs da{a.fp, a.ip, &a.ga, &a.gb, a.kind, a.fm, a.zslow, a.zslowf};
-    make_dist_a<D>(da, sm, d);
+    make_dist_a<D == FAM_FIXED ? FAM_LEMIRE : D>(da, sm, d);
     typedef typename DT::out_t T;
-    __shared__ __align__(16) unsigned char ring_sm[32 * BLOCK];
-    RingWriter<T, BLOCK> wr;
-    wr.init((T *)a.out, j * a.nper, (T *)ring_sm + threadIdx.x);
+    typename std::conditional<sizeof(T) == 8, VecWriter8<T>, ScalarWriter<T>>::type wr;
+    wr.init((T *)a.out, j * a.nper);
     Tally tl;
     if constexpr (D == FAM_LEMIRE) {
         for (u64 i = 0; i < a.nper;) {
@@ -1227,7 +1301,7 @@ struct DevCtx {
     size_t cub_bytes = 0;
     DevResult *res = nullptr;
     DevResult *res_host = nullptr;
-    std::map<std::pair<u64, int>, u64 *> x256_ml;  // (L, levels) -> matrices
+    std::map<std::tuple<int, u64, int>, u64 *> x256_ml;  // (family, L, levels) -> matrices
     void *stage = nullptr;
     size_t stage_bytes = 0;
     cublasHandle_t blas = nullptr;
@@ -1303,16 +1377,19 @@ rs_status ensure_scratch(DevCtx &c, size_t T) {
 }
 
 // x256: ML[0] = T^L, ML[1 + k] = T^(32 L 2^k) for k < levels; cached per (L, levels) on the device
-rs_status x256_mats(DevCtx &c, u64 L, int levels, u64 **out) {
-    auto key = std::make_pair(L, levels);
+rs_status x256_mats(DevCtx &c, int engine, u64 L, int levels, u64 **out) {
+    // x256 family, or the 128-bit xorshift128+ / xoroshiro128 matrices padded to 256 bits
+    const bool narrow = engine == RS_ENG_X128P || engine == RS_ENG_XORO;
+    auto pow2 = [&](int k) -> const rs::Mat256 & { return narrow ? rs::x128_pow2(engine, k) : rs::x256_pow2(k); };
+    auto key = std::make_tuple(narrow ? engine : 0, L, levels);
     auto it = c.x256_ml.find(key);
     if (it != c.x256_ml.end()) { *out = it->second; return RS_OK; }
     std::vector<rs::Mat256> m(1 + levels);
     bool init = false;
     for (int k = 0; k < 64; k++)
         if ((L >> k) & 1) {
-            if (!init) { m[0] = rs::x256_pow2(k); init = true; }
-            else rs::mat_mul(rs::x256_pow2(k), m[0], m[0]);
+            if (!init) { m[0] = pow2(k); init = true; }
+            else rs::mat_mul(pow2(k), m[0], m[0]);
         }
     if (levels > 0) {
         rs::Mat256 *t = new rs::Mat256(m[0]);
@@ -1383,10 +1460,15 @@ VarKernels var_kernels_e(int fam) {
     default: return var_kernels_ed<E, FAM_LEMIRE>();
     }
 }
+// Engines whose parse passes read materialized words: the expensive ones (Philox,
+// ranlux++, ChaCha20), the interleaved ones, and the registry's other skip-ahead
+// engines (x128+, xoro++, squares), which thereby need no parse-kernel instantiations.
 bool parse_from_memory(int e) {
-    return e == RS_ENG_PHILOX || e == RS_ENG_RANLUX || e == RS_ENG_X256PP_SIMD || e == RS_ENG_X256SS_SIMD;
+    return e == RS_ENG_PHILOX || e == RS_ENG_RANLUX || e == RS_ENG_X256PP_SIMD || e == RS_ENG_X256SS_SIMD ||
+           e == RS_ENG_CHACHA20 || e == RS_ENG_X128P || e == RS_ENG_XORO || e == RS_ENG_SQUARES;
 }
-bool is_serial(int e) { return e == RS_ENG_SFC64 || e == RS_ENG_SFC64_SIMD; }
+// no skip-ahead: one device thread replays the stream (sfc64 rng.py:162-163; cwg128 likewise)
+bool is_serial(int e) { return e == RS_ENG_SFC64 || e == RS_ENG_SFC64_SIMD || e == RS_ENG_CWG128; }
 VarKernels var_kernels(int e, int fam) {
     switch (e) {
     case RS_ENG_X256SS: return var_kernels_e<RS_ENG_X256SS>(fam);
@@ -1412,6 +1494,10 @@ const void *fixed_kernel(int e, int mode) {
     case RS_ENG_X256PP: return fixed_kernel_e<RS_ENG_X256PP>(mode);
     case RS_ENG_PCG64: return fixed_kernel_e<RS_ENG_PCG64>(mode);
     case RS_ENG_PHILOX: return fixed_kernel_e<RS_ENG_PHILOX>(mode);
+    case RS_ENG_X128P: return fixed_kernel_e<RS_ENG_X128P>(mode);
+    case RS_ENG_XORO: return fixed_kernel_e<RS_ENG_XORO>(mode);
+    case RS_ENG_SQUARES: return fixed_kernel_e<RS_ENG_SQUARES>(mode);
+    case RS_ENG_CHACHA20: return fixed_kernel_e<RS_ENG_CHACHA20>(mode);
     default: return fixed_kernel_e<RS_ENG_RANLUX>(mode);
     }
 }
@@ -1443,6 +1529,7 @@ const void *serial_kernel_e(int fam, int fixed_mode) {
     }
 }
 const void *serial_kernel(int engine, int fam, int fixed_mode) {
+    if (engine == RS_ENG_CWG128) return serial_kernel_e<RS_ENG_CWG128>(fam, fixed_mode);
     return engine == RS_ENG_SFC64_SIMD ? serial_kernel_e<RS_ENG_SFC64_SIMD>(fam, fixed_mode)
                                        : serial_kernel_e<RS_ENG_SFC64>(fam, fixed_mode);
 }
@@ -1708,11 +1795,20 @@ rs_status plan_segments(DevCtx &c, FillPlan &p, u64 words, u64 Lmin, int occ, cu
         }
     } else if (p.engine == RS_ENG_RANLUX) {
         for (int j = 0; j < levels; j++) rs::rlx_pow_A((u128)(L / 9) << j, p.rlx[j]);
-    } else if (p.engine == RS_ENG_X256SS || p.engine == RS_ENG_X256PP) {
+    } else if (p.engine == RS_ENG_CHACHA20) {
+        if ((p.base[5] >> 32) + (u128)T * (L / 8) > ((u128)1 << 32)) {
+            rs::set_error("chacha20 stream exhausted");  // counter.py:212-213
+            return RS_ERR_VALUE;
+        }
+    } else if (p.engine == RS_ENG_X256SS || p.engine == RS_ENG_X256PP || p.engine == RS_ENG_X128P ||
+               p.engine == RS_ENG_XORO) {
         int lv = 0;  // bits of the warp index
         while ((1ULL << lv) < T / 32) lv++;
         u64 *ml;
-        s = x256_mats(c, L, lv, &ml);
+        if (p.engine == RS_ENG_X128P || p.engine == RS_ENG_XORO) {  // padded 4-word states
+            p.base[2] = p.base[3] = 0;
+        }
+        s = x256_mats(c, p.engine, L, lv, &ml);
         if (s) return s;
         p.x256_states = c.states;
         void *args[] = {&p, &ml, &c.states};
@@ -1795,7 +1891,7 @@ rs_status launch_simd(DevCtx &c, FillPlan &p, int mode, cudaStream_t st) {
     int lv = 0;
     while ((1ULL << lv) < Gpad / 32) lv++;
     u64 *ml;
-    if ((rc = x256_mats(c, Ls, lv, &ml))) return rc;
+    if ((rc = x256_mats(c, RS_ENG_X256PP, Ls, lv, &ml))) return rc;
     p.x256_states = c.states;
     void *sargs[] = {&p, &ml, &c.states};
     if ((rc = launch((const void *)k_x256_setup, dim3((unsigned)(Gpad / BLOCK), 8), dim3(BLOCK), sargs, st))) return rc;
@@ -1952,7 +2048,7 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
             // materialize the chunk's engine words (+ slack for the parses that run past the
             // last segment end) with the coalesced fixed-fill kernel
             u64 nw = (u64)p.T * p.L + std::max<u64>(1ULL << 16, (u64)p.T * p.L / 64);
-            nw = (nw + 35) / 36 * 36;
+            nw = (nw + 143) / 144 * 144;
             if (nw * 8 > c.words_bytes) {
                 cudaFree(c.words);
                 c.words = nullptr;
@@ -2025,7 +2121,7 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
         }
         done += total;
         u64 resume = c.res_host->next_start + to_engine;  // engine unit of the next boundary
-        origin = resume / u / 36 * 36;
+        origin = resume / u / 72 * 72;  // whole Philox / ranlux / 8-word blocks
         lp0 = resume - u * origin;
         first = false;
     }
@@ -2164,8 +2260,9 @@ rs_status rs_fill_streams(int32_t engine, const uint64_t *seed, int32_t n_seed, 
                           const uint64_t *iparams, uint64_t n_per_stream, void *out, void *cuda_stream) {
     std::lock_guard<std::mutex> g(g_mu);
     if (engine != RS_ENG_SFC64 && engine != RS_ENG_PCG64 && engine != RS_ENG_PHILOX && engine != RS_ENG_X256SS &&
-        engine != RS_ENG_X256PP) {
-        rs::set_error("per-stream mode supports sfc64, pcg64, philox, x256**, x256++");
+        engine != RS_ENG_X256PP && engine != RS_ENG_X128P && engine != RS_ENG_XORO && engine != RS_ENG_SQUARES &&
+        engine != RS_ENG_CHACHA20 && engine != RS_ENG_CWG128) {
+        rs::set_error("per-stream mode supports sfc64, pcg64, philox, x256**, x256++, x128+, xoro++, squares, chacha20, cwg128");
         return RS_ERR_UNSUPPORTED;
     }
     if (n_seed < 0 || n_seed > 16 || n_prefix < 0 || n_prefix > 7) {
@@ -2228,9 +2325,10 @@ rs_status rs_fill_streams(int32_t engine, const uint64_t *seed, int32_t n_seed, 
         a.ip[1] = 0;
         a.ip[2] = 0;
         a.ip[3] = r.ip[1];
-    } else if (r.fixed_mode >= 0) {
-        rs::set_error("per-stream mode covers the variable-consumption samplers and bounds b >= 1");
-        return RS_ERR_UNSUPPORTED;
+    } else if (r.fixed_mode >= 0) {  // raw / u01 / u01f / unif / gumbel / masks / full spans
+        d = FAM_FIXED;
+        a.fmode = r.fixed_mode;
+        memcpy(a.ip, r.ip, sizeof a.ip);
     }
     const void *fn = nullptr;
 #define RS_STREAM_CASE(E)                                                     \
@@ -2240,12 +2338,18 @@ rs_status rs_fill_streams(int32_t engine, const uint64_t *seed, int32_t n_seed, 
     case FAM_GAMMA: fn = (const void *)k_streams<E, FAM_GAMMA>; break;        \
     case FAM_F32: fn = (const void *)k_streams<E, FAM_F32>; break;            \
     case FAM_U32: fn = (const void *)k_streams<E, FAM_U32>; break;            \
+    case FAM_FIXED: fn = (const void *)k_streams<E, FAM_FIXED>; break;        \
     default: fn = (const void *)k_streams<E, FAM_LEMIRE>; break;              \
     }
     if (engine == RS_ENG_SFC64) { RS_STREAM_CASE(RS_ENG_SFC64) }
     else if (engine == RS_ENG_PCG64) { RS_STREAM_CASE(RS_ENG_PCG64) }
     else if (engine == RS_ENG_PHILOX) { RS_STREAM_CASE(RS_ENG_PHILOX) }
     else if (engine == RS_ENG_X256SS) { RS_STREAM_CASE(RS_ENG_X256SS) }
+    else if (engine == RS_ENG_X128P) { RS_STREAM_CASE(RS_ENG_X128P) }
+    else if (engine == RS_ENG_XORO) { RS_STREAM_CASE(RS_ENG_XORO) }
+    else if (engine == RS_ENG_SQUARES) { RS_STREAM_CASE(RS_ENG_SQUARES) }
+    else if (engine == RS_ENG_CHACHA20) { RS_STREAM_CASE(RS_ENG_CHACHA20) }
+    else if (engine == RS_ENG_CWG128) { RS_STREAM_CASE(RS_ENG_CWG128) }
     else { RS_STREAM_CASE(RS_ENG_X256PP) }
 #undef RS_STREAM_CASE
     void *args[] = {&a};

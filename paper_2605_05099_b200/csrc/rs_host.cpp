@@ -15,20 +15,25 @@ static thread_local std::string g_err;
 void set_error(const std::string &m) { g_err = m; }
 void clear_error() { g_err.clear(); }
 
-int state_words(int e) {
+int state_words(int e) {  // engines/*.py STATE_WORDS
     switch (e) {
     case RS_ENG_X256PP: case RS_ENG_X256SS: case RS_ENG_PCG64: case RS_ENG_SFC64: return 4;
-    case RS_ENG_PHILOX: return 6;
+    case RS_ENG_X128P: case RS_ENG_XORO: case RS_ENG_SQUARES: return 2;
+    case RS_ENG_PHILOX: case RS_ENG_CHACHA20: return 6;
+    case RS_ENG_CWG128: return 8;
     case RS_ENG_RANLUX: return 9;
     case RS_ENG_X256PP_SIMD: case RS_ENG_X256SS_SIMD: case RS_ENG_SFC64_SIMD: return 32;
     default: return 0;
     }
 }
-int seed_words(int e) {
+int seed_words(int e) {  // engines/*.py SEED_WORDS
     switch (e) {
     case RS_ENG_X256PP: case RS_ENG_X256SS: case RS_ENG_PCG64: return 4;
-    case RS_ENG_PHILOX: return 2;
+    case RS_ENG_PHILOX: case RS_ENG_X128P: case RS_ENG_XORO: return 2;
+    case RS_ENG_SQUARES: return 1;
     case RS_ENG_SFC64: case RS_ENG_SFC64_SIMD: return 3;
+    case RS_ENG_CHACHA20: return 6;
+    case RS_ENG_CWG128: return 8;
     case RS_ENG_RANLUX: return 9;
     case RS_ENG_X256PP_SIMD: case RS_ENG_X256SS_SIMD: return 4;
     default: return 0;
@@ -38,7 +43,7 @@ int chunk(int e) {
     switch (e) {
     case RS_ENG_PHILOX: return 4;
     case RS_ENG_RANLUX: return 9;
-    case RS_ENG_X256PP_SIMD: case RS_ENG_X256SS_SIMD: case RS_ENG_SFC64_SIMD: return 8;
+    case RS_ENG_X256PP_SIMD: case RS_ENG_X256SS_SIMD: case RS_ENG_SFC64_SIMD: case RS_ENG_CHACHA20: return 8;
     default: return 1;
     }
 }
@@ -104,6 +109,91 @@ void x256_advance(uint64_t s[4], u128 n) {
             mat_vec(x256_pow2(k), s, o);
             memcpy(s, o, 32);
         }
+}
+
+// ------------------------------------------------------------------ xorshift128+ / xoroshiro128
+// (xorfam.py:29-42, 127-170). Their 128-bit linear steps reuse the 256-bit matrix
+// type with words 2 and 3 (and columns 128..255) left zero.
+void x128p_step_host(uint64_t s[2]) {  // xorfam.py:29-34
+    uint64_t s1 = s[0], s0 = s[1];
+    s1 ^= s1 << 23;
+    s[0] = s0;
+    s[1] = s1 ^ s0 ^ (s1 >> 18) ^ (s0 >> 5);
+}
+void xoro_step_host(uint64_t s[2]) {  // xorfam.py:37-42
+    uint64_t s0 = s[0], s1 = s[1] ^ s[0];
+    s[0] = rotl(s0, 49) ^ s1 ^ (s1 << 21);
+    s[1] = rotl(s1, 28);
+}
+static std::vector<Mat256> *g_x128_pow2[2] = {nullptr, nullptr};
+static std::once_flag g_x128_once[2];
+static void build_x128_table(int f) {  // f = 0: x128+, 1: xoro
+    g_x128_pow2[f] = new std::vector<Mat256>(128);
+    Mat256 &t = (*g_x128_pow2[f])[0];
+    memset(&t, 0, sizeof t);
+    for (int j = 0; j < 128; j++) {
+        uint64_t v[2] = {0, 0};
+        v[j / 64] = 1ULL << (j % 64);
+        if (f == 0) x128p_step_host(v); else xoro_step_host(v);
+        t.col[j][0] = v[0];
+        t.col[j][1] = v[1];
+    }
+    for (int k = 1; k < 128; k++) mat_mul((*g_x128_pow2[f])[k - 1], (*g_x128_pow2[f])[k - 1], (*g_x128_pow2[f])[k]);
+}
+const Mat256 &x128_pow2(int e, int k) {
+    int f = e == RS_ENG_XORO ? 1 : 0;
+    std::call_once(g_x128_once[f], build_x128_table, f);
+    return (*g_x128_pow2[f])[k];
+}
+void x128_advance(int e, uint64_t s[2], u128 n) {
+    if (n < 64) {
+        for (int i = 0; i < (int)n; i++) { if (e == RS_ENG_XORO) xoro_step_host(s); else x128p_step_host(s); }
+        return;
+    }
+    for (int k = 0; k < 128 && n; k++, n >>= 1)
+        if (n & 1) {
+            uint64_t in[4] = {s[0], s[1], 0, 0}, o[4];
+            mat_vec(x128_pow2(e, k), in, o);
+            s[0] = o[0];
+            s[1] = o[1];
+        }
+}
+
+// squares64, counter.py:12-48: word = f(counter * key), one per counter value
+static inline uint64_t sq_swap(uint64_t x) { return (x >> 32) | (x << 32); }
+uint64_t squares_word(uint64_t ctr, uint64_t key) {
+    uint64_t x = ctr * key, y = x, z = y + key;
+    x = sq_swap(x * x + y);
+    x = sq_swap(x * x + z);
+    x = sq_swap(x * x + y);
+    uint64_t t = x = x * x + z;
+    x = sq_swap(x);
+    return t ^ ((x * x + y) >> 32);
+}
+
+// ChaCha20, counter.py:170-207: state words [k0..k3, nonce0|nonce1<<32, nonce2|counter<<32]
+static inline uint32_t rotl32(uint32_t x, int r) { return (x << r) | (x >> (32 - r)); }
+void chacha_block(const uint64_t *s, uint32_t counter, uint64_t *out) {
+    uint32_t st[16] = {0x61707865u, 0x3320646Eu, 0x79622D32u, 0x6B206574u};
+    for (int i = 0; i < 4; i++) { st[4 + 2 * i] = (uint32_t)s[i]; st[5 + 2 * i] = (uint32_t)(s[i] >> 32); }
+    st[12] = counter;
+    st[13] = (uint32_t)s[4];
+    st[14] = (uint32_t)(s[4] >> 32);
+    st[15] = (uint32_t)s[5];
+    uint32_t x[16];
+    memcpy(x, st, sizeof x);
+    static const int QR[8][4] = {{0, 4, 8, 12}, {1, 5, 9, 13}, {2, 6, 10, 14}, {3, 7, 11, 15},
+                                 {0, 5, 10, 15}, {1, 6, 11, 12}, {2, 7, 8, 13}, {3, 4, 9, 14}};
+    for (int r = 0; r < 10; r++)
+        for (int q = 0; q < 8; q++) {
+            uint32_t &a = x[QR[q][0]], &b = x[QR[q][1]], &c = x[QR[q][2]], &d = x[QR[q][3]];
+            a += b; d = rotl32(d ^ a, 16);
+            c += d; b = rotl32(b ^ c, 12);
+            a += b; d = rotl32(d ^ a, 8);
+            c += d; b = rotl32(b ^ c, 7);
+        }
+    for (int i = 0; i < 8; i++)
+        out[i] = (uint64_t)(x[2 * i] + st[2 * i]) | ((uint64_t)(x[2 * i + 1] + st[2 * i + 1]) << 32);
 }
 
 // ------------------------------------------------------------------ PCG64
@@ -282,6 +372,35 @@ void engine_generate(int e, uint64_t *s, uint64_t *out, int n) {
         for (int c = 0; c < n / 9; c++) { rlx_mulmod(s, A, s); memcpy(out + 9 * c, s, 72); }
         break;
     }
+    case RS_ENG_X128P:  // xorfam.py:137-146
+        for (int i = 0; i < n; i++) { out[i] = s[0] + s[1]; x128p_step_host(s); }
+        break;
+    case RS_ENG_XORO:  // xorfam.py:160-168
+        for (int i = 0; i < n; i++) { out[i] = rotl(s[0] + s[1], 17) + s[0]; xoro_step_host(s); }
+        break;
+    case RS_ENG_SQUARES:  // state [counter, key]
+        for (int i = 0; i < n; i++) out[i] = squares_word(s[0]++, s[1]);
+        break;
+    case RS_ENG_CHACHA20:  // the caller checked the 32-bit block counter (counter.py:209-216)
+        for (int b = 0; b < n / 8; b++) {
+            uint32_t ctr = (uint32_t)(s[5] >> 32);
+            chacha_block(s, ctr, out + 8 * b);
+            s[5] = (s[5] & 0xFFFFFFFFULL) | ((uint64_t)(ctr + 1) << 32);
+        }
+        break;
+    case RS_ENG_CWG128: {  // cwg.py:28-36: state words x, weyl, extra, inc (lo, hi each)
+        u128 x = ((u128)s[1] << 64) | s[0], weyl = ((u128)s[3] << 64) | s[2];
+        u128 extra = ((u128)s[5] << 64) | s[4], inc = ((u128)s[7] << 64) | s[6];
+        for (int i = 0; i < n; i++) {
+            weyl += x;
+            extra += inc;
+            x = ((x >> 1) * (weyl | 1)) ^ extra;
+            out[i] = (uint64_t)(weyl >> 96) ^ (uint64_t)x;
+        }
+        s[0] = (uint64_t)x; s[1] = (uint64_t)(x >> 64); s[2] = (uint64_t)weyl; s[3] = (uint64_t)(weyl >> 64);
+        s[4] = (uint64_t)extra; s[5] = (uint64_t)(extra >> 64);
+        break;
+    }
     case RS_ENG_X256PP_SIMD: case RS_ENG_X256SS_SIMD: case RS_ENG_SFC64_SIMD: {
         // interleave.py:71-76: word i = lane (i mod 8) at step i / 8; state is lane-major
         int base = e == RS_ENG_X256PP_SIMD ? RS_ENG_X256PP : e == RS_ENG_X256SS_SIMD ? RS_ENG_X256SS : RS_ENG_SFC64;
@@ -314,7 +433,17 @@ bool engine_advance_words(int e, uint64_t *s, u128 words) {
         rlx_mulmod(s, p, s);
         return true;
     }
-    default: return false;  // sfc64 has no skip-ahead (rng.py:162-163)
+    case RS_ENG_X128P: case RS_ENG_XORO: x128_advance(e, s, words); return true;
+    case RS_ENG_SQUARES: s[0] += (uint64_t)words; return true;
+    case RS_ENG_CHACHA20: {  // 32-bit block counter: positions up to block 2^32 exist
+        if (words % 8) return false;
+        u128 c = (u128)(s[5] >> 32) + words / 8;
+        if (c > ((u128)1 << 32)) return false;
+        if (c == ((u128)1 << 32)) return false;  // not representable in the state word
+        s[5] = (s[5] & 0xFFFFFFFFULL) | ((uint64_t)c << 32);
+        return true;
+    }
+    default: return false;  // sfc64 / cwg128 have no skip-ahead (rng.py:162-163)
     }
 }
 
@@ -384,6 +513,16 @@ void engine_seed_from(int e, const uint64_t *w, uint64_t *s) {
     case RS_ENG_PHILOX: s[0] = s[1] = s[2] = s[3] = 0; s[4] = w[0]; s[5] = w[1]; break;  // counter.py:139-141
     case RS_ENG_SFC64: s[0] = w[0]; s[1] = w[1]; s[2] = w[2]; s[3] = 1; break;  // sfc.py:53-55
     case RS_ENG_RANLUX: rlx_reduce_seed(w, s); break;  // ranlux.py:106-110
+    case RS_ENG_X128P: case RS_ENG_XORO:  // xorfam.py:66-70
+        s[0] = w[0]; s[1] = w[1];
+        if (!(s[0] | s[1])) s[0] = 1;
+        break;
+    case RS_ENG_SQUARES: s[0] = 0; s[1] = w[0]; break;  // counter.py:63-65
+    case RS_ENG_CHACHA20:  // counter.py:228-233: key, 96-bit nonce, counter 0
+        memcpy(s, w, 40);
+        s[5] = w[5] & 0xFFFFFFFFULL;
+        break;
+    case RS_ENG_CWG128: memcpy(s, w, 64); s[6] |= 1; break;  // cwg.py:62-67
     }
 }
 
@@ -440,6 +579,13 @@ rs_status rs_engine_check_state(int32_t e, const uint64_t *w) {
                 set_error("lane " + std::to_string(k) + " state must not be all zero");
                 return RS_ERR_VALUE;
             }
+    } else if (e == RS_ENG_X128P || e == RS_ENG_XORO) {
+        if (!(w[0] | w[1])) {
+            set_error(std::string("all-zero state is invalid for ") + (e == RS_ENG_X128P ? "x128+" : "xoro++"));
+            return RS_ERR_VALUE;
+        }
+    } else if (e == RS_ENG_CWG128) {  // cwg.py:56-57
+        if (!(w[6] & 1)) { set_error("cwg128 Weyl increment must be odd"); return RS_ERR_VALUE; }
     } else if (e == RS_ENG_PCG64) {
         if (!(w[2] & 1)) { set_error("pcg64 increment must be odd"); return RS_ERR_VALUE; }
     } else if (e == RS_ENG_RANLUX) {
@@ -455,6 +601,10 @@ rs_status rs_engine_check_state(int32_t e, const uint64_t *w) {
 rs_status rs_engine_generate(int32_t e, uint64_t *state, uint64_t *out, int32_t n) {
     if (!known_engine(e)) { set_error("engine not on the B200 path"); return RS_ERR_UNSUPPORTED; }
     if (n < 0 || n % chunk(e)) { set_error("generate count must be a multiple of the engine chunk"); return RS_ERR_VALUE; }
+    if (e == RS_ENG_CHACHA20 && (state[5] >> 32) + (uint64_t)(n / 8) > 0xFFFFFFFFULL + 1) {
+        set_error("chacha20 stream exhausted");  // counter.py:212-213 (OverflowError)
+        return RS_ERR_VALUE;
+    }
     engine_generate(e, state, out, n);
     clear_error();
     return RS_OK;
@@ -486,6 +636,14 @@ rs_status rs_engine_jump(int32_t e, uint64_t *state, int32_t k) {
         uint64_t p[9];
         rlx_pow2k_A(k, p);
         rlx_mulmod(state, p, state);
+        break;
+    }
+    case RS_ENG_X128P: case RS_ENG_XORO: {  // 2^k steps, jumps.py FAMILY_JUMPS (k < 128)
+        if (k >= 128) { set_error("jump exponent out of range"); return RS_ERR_VALUE; }
+        uint64_t in[4] = {state[0], state[1], 0, 0}, o[4];
+        mat_vec(x128_pow2(e, k), in, o);
+        state[0] = o[0];
+        state[1] = o[1];
         break;
     }
     default:

@@ -33,6 +33,9 @@ void mat_vec(const Mat256 &m, const uint64_t in[4], uint64_t out[4]);
 void mat_mul(const Mat256 &a, const Mat256 &b, Mat256 &out);  // out = a*b
 void x256_advance(uint64_t s[4], u128 n);                      // n steps
 void x256_step_host(uint64_t s[4]);
+// xorshift128+ / xoroshiro128: T^(2^k) as 256-bit matrices with words 2, 3 zero (k < 128)
+const Mat256 &x128_pow2(int engine, int k);
+void x128_advance(int engine, uint64_t s[2], u128 n);
 
 // ---- PCG64-DXSM LCG (pcg.py:41-55)
 static const uint64_t PCG_MULT = 0xDA942042E4DD58B5ULL;

@@ -78,6 +78,12 @@ class Engine:
             self.s = [0, 0, 0, 1]
         elif eid == "ranlux++":
             self.s[0] = 1
+        elif eid in ("x128+", "xoro++"):  # xorfam.py:52-54
+            self.s[0] = 1
+        elif eid == "squares":  # counter.py:23-25: counter 0, key 1
+            self.s = [0, 1]
+        elif eid == "cwg128":  # cwg.py:22-26: x = weyl = extra = 0, inc = 1
+            self.s = [0, 0, 0, 0, 0, 0, 1, 0]
         elif eid in ("x256++simd", "x256**simd"):  # lane k = [4k+1, 4k+2, 4k+3, 4k+4]
             self.s = [4 * k + w + 1 for k in range(8) for w in range(4)]
         elif eid == "sfc64simd":  # lanes from a default sfc64 (a=b=c=0, w=1), counters + k*2^61
@@ -114,10 +120,28 @@ class Engine:
         self.s[2] = int(words[0]) & MASK64 | 1
         self.s[3] = int(words[1]) & MASK64
 
-    def set_key(self, words):  # counter.py:123-127
+    def set_key(self, words):  # philox counter.py:123-127; squares counter.py:50-54
+        if self.ID == "squares":
+            if len(words) != 1:
+                raise ValueError("squares key is 1 word")
+            self.s = [0, int(words[0]) & MASK64]
+            return
         if len(words) != 2:
             raise ValueError("philox key is 2 words")
         self.s = [0, 0, 0, 0, int(words[0]) & MASK64, int(words[1]) & MASK64]
+
+    def set_weyl(self, words):  # cwg.py:40-45: odd increment, then a 96-word warm-up
+        if len(words) != 2:
+            raise ValueError("cwg128 Weyl increment is 2 words")
+        self.s[6] = (int(words[0]) & MASK64) | 1
+        self.s[7] = int(words[1]) & MASK64
+        self.generate(96)
+
+    def set_nonce(self, words):  # counter.py:218-224: 96-bit nonce, counter 0
+        if len(words) != 2:
+            raise ValueError("chacha20 nonce is 96 bits passed as 2 words")
+        self.s[4] = int(words[0]) & MASK64
+        self.s[5] = int(words[1]) & 0xFFFFFFFF
 
     def set_abc(self, words):  # sfc.py:38-43: (a, b, c), w = 0, 18-step warmup
         if len(words) != 3:
@@ -142,8 +166,7 @@ def make(selector=None):
     row = next(r for r in _REGISTRY if r[0] == eid)
     if not _lib.lib.rs_engine_supported(row[9]):
         raise NotImplementedError(
-            "engine %r is not on the B200 fill path (supported: x256**, x256++, pcg64, philox, sfc64, ranlux++, "
-            "x256++simd, x256**simd, sfc64simd)"
+            "engine %r is not on the B200 fill path"
             % eid)
     return Engine(*row)
 

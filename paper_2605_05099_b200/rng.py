@@ -27,6 +27,8 @@ MASK64 = 0xFFFFFFFFFFFFFFFF
 
 _POLY_JUMP = {"x256++", "x256**", "x256++simd", "x256**simd"}
 STANDARD_JUMPS = (32, 64, 96, 128, 192)  # jumps.py:24
+_NARROW_JUMP = {"x128+": "x128+", "xoro++": "xoro"}  # rng.py:20-25 -> jumps.py:25-29 families
+_NARROW_JUMPS = (32, 64, 96)
 _STREAM_METHODS = {  # rng.py:27-35
     "pcg64": ("set_inc", 2),
     "squares": ("set_key", 1),
@@ -185,13 +187,16 @@ class Rng:
 
     @_op
     def jump(self, k):
-        """rng.py:135-164: x256 family 2^k steps (k in the committed table), pcg64
-        advance(2^k), ranlux++ x*A^(2^k); others raise."""
+        """rng.py:135-164: x256 / x128+ / xoro families 2^k steps (k in the committed
+        table), pcg64 advance(2^k), ranlux++ x*A^(2^k); others raise."""
         k = int(k)
         eid = self.engine_id
         if eid in _POLY_JUMP:
             if k not in STANDARD_JUMPS + (253,):
                 raise ValueError("no jump polynomial for family 'x256' at 2^%d" % k)
+        elif eid in _NARROW_JUMP:  # jumps.py:179-188
+            if k not in _NARROW_JUMPS:
+                raise ValueError("no jump polynomial for family %r at 2^%d" % (_NARROW_JUMP[eid], k))
         elif eid in ("pcg64", "ranlux++"):
             if k not in STANDARD_JUMPS:
                 raise ValueError("%s jump exponent must be one of %s" % (eid, STANDARD_JUMPS))

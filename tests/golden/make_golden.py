@@ -107,7 +107,8 @@ case("default_engine_raw", None, [2024], "uint64", {}, 1 << 16, keep=False)
 case("default_engine_norm", None, [2024], "norm", {}, 1 << 16, keep=False)
 
 # edge cases: empty / single / parameters / modes / mid-buffer starts
-ENG = ("x256**", "x256++", "pcg64", "philox", "sfc64", "ranlux++", "x256++simd", "x256**simd", "sfc64simd")
+ENG = ("x256**", "x256++", "pcg64", "philox", "sfc64", "ranlux++", "x256++simd", "x256**simd", "sfc64simd",
+       "x128+", "xoro++", "squares", "cwg128", "chacha20")
 for e in ENG:
     tag = e.replace("+", "p").replace("*", "s")
     case("edge_%s_n0" % tag, e, [5], "norm", {}, 0)
@@ -140,7 +141,7 @@ DERIVED = [("unif", {"a": -2.0, "b": 3.0}), ("unif", {}), ("uniff", {"a": -2.0, 
            ("int", {}), ("int", {"m": -(1 << 31), "n": 0}), ("long_long", {"m": -10 ** 15, "n": 10 ** 18}),
            ("long_long", {}), ("long_long", {"m": 7, "n": 7 + (1 << 40) - 1})]
 TRANSFORMED = ("lognormal", "gumbel", "pareto", "weibull", "gpd")
-for e in ("x256**", "pcg64", "philox", "sfc64", "ranlux++", "x256++simd"):
+for e in ("x256**", "pcg64", "philox", "sfc64", "ranlux++", "x256++simd", "xoro++", "chacha20", "cwg128"):
     tag = e.replace("+", "p").replace("*", "s")
     for i, (dist, params) in enumerate(DERIVED):
         case("derived_%s_%s_%d" % (tag, dist, i), e, [100 + i], dist, params, 1500, pre=[("u32", 1)],
@@ -244,11 +245,30 @@ def main():
             r.jump(k)
             jstates.append({"engine": e, "k": k, "state": ["%016x" % w for w in r.get_state()],
                             "next": ["%016x" % r.next_u64() for _ in range(5)]})
+    for e in ("x128+", "xoro++"):  # jumps.py FAMILY_JUMPS for the 128-bit families
+        for k in (32, 64, 96):
+            r = state_io.create(e, seed=[77])
+            r.next_u64()
+            r.jump(k)
+            jstates.append({"engine": e, "k": k, "state": ["%016x" % w for w in r.get_state()],
+                            "next": ["%016x" % r.next_u64() for _ in range(5)]})
     r = state_io.create("pcg64", seed=[77])
     r.advance(123456789012345)
     jstates.append({"engine": "pcg64", "advance": "123456789012345", "state": ["%016x" % w for w in r.get_state()],
                     "next": ["%016x" % r.next_u64() for _ in range(5)]})
     out["jumps"] = jstates
+
+    # stream selection (rng.py:27-35, 173-188) for every engine that has one
+    streams = []
+    for e, words in (("pcg64", [5, 6]), ("squares", [123]), ("philox", [9, 10]), ("sfc64", [1, 2, 3]),
+                     ("sfc64simd", [1, 2, 3]), ("cwg128", [5, 6]), ("chacha20", [9, 10])):
+        r = state_io.create(e, seed=[88])
+        r.next_u32()
+        r.set_stream(words)
+        streams.append({"engine": e, "words": ["%016x" % w for w in words],
+                        "state": ["%016x" % w for w in r.get_state()],
+                        "next": ["%016x" % r.next_u64() for _ in range(20)]})
+    out["streams"] = streams
 
     # multivariate normal (config 5a, scaled down): S from the same philox stream
     d, n = 16, 64

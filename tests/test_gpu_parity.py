@@ -14,7 +14,8 @@ from conftest import golden_params, is_vectorized, vec_close
 
 pytestmark = pytest.mark.gpu
 
-ENGINES = ("x256**", "x256++", "pcg64", "philox", "sfc64", "ranlux++", "x256++simd", "x256**simd", "sfc64simd")
+ENGINES = ("x256**", "x256++", "pcg64", "philox", "sfc64", "ranlux++", "x256++simd", "x256**simd", "sfc64simd",
+           "x128+", "xoro++", "squares", "cwg128", "chacha20")
 
 
 def _h(ws):
@@ -108,6 +109,17 @@ CASES = [
     ("x256++simd", "norm", {}, 1 << 21),
     ("x256**simd", "gamma", {"alpha": 0.4}, 1 << 19),
     ("sfc64simd", "norm", {}, 1 << 14),
+    ("x128+", "uint64", {}, (1 << 21) + 7),
+    ("x128+", "norm", {}, 1 << 20),
+    ("xoro++", "u01f", {}, (1 << 21) + 1),
+    ("xoro++", "gamma", {"alpha": 2.5}, 1 << 19),
+    ("squares", "u01", {}, 1 << 21),
+    ("squares", "exp", {}, 1 << 20),
+    ("chacha20", "uint64", {}, (1 << 21) + 5),
+    ("chacha20", "norm", {}, 1 << 20),
+    ("chacha20", "uint64", {"b": 1000003}, 1 << 20),
+    ("cwg128", "norm", {}, 1 << 14),
+    ("cwg128", "u01f", {}, (1 << 14) + 1),
 ]
 
 
@@ -175,7 +187,7 @@ def test_streams_half_and_transform_families():
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 35, 36, 37, 143, 144, 145, 1000, 4097, 65536 + 7])
-@pytest.mark.parametrize("engine", ["x256**", "pcg64", "philox", "ranlux++", "x256++simd"])
+@pytest.mark.parametrize("engine", ["x256**", "pcg64", "philox", "ranlux++", "x256++simd", "xoro++", "chacha20"])
 def test_small_and_ragged(engine, n):
     for dist, params in (("uint64", {}), ("u01f", {}), ("norm", {}), ("gamma", {"alpha": 0.7}),
                          ("uint64", {"b": 3}), ("normf", {}), ("uint32", {"b": 3}), ("int", {}), ("uniff", {})):
@@ -219,6 +231,18 @@ def test_streams_c5b(golden, m):
     for j in (3, 500, S - 1):
         o = O.OracleRng("sfc64", seed=[31], spawn_key=(j,))
         assert np.array_equal(out[j], o.fill("uint64", {"b": m}, 4096))
+
+
+@pytest.mark.parametrize("engine", ["pcg64", "philox", "x256**", "x128+", "xoro++", "squares", "chacha20", "cwg128"])
+def test_streams_every_engine(engine):
+    """per-stream mode: stream j = create(engine, seed, spawn_key=prefix + (j0 + j,)) for
+    every engine with a device seeding path (cwg128's only parallel mode)."""
+    for dist, params, n in (("uint64", {}, 1001), ("norm", {"mu": 2.0}, 777), ("u01f", {}, 515),
+                            ("gamma", {"alpha": 1.5}, 300), ("uint64", {"b": 6}, 400)):
+        out = _np(fill_streams(engine, [7], [4], 5, 96, dist, params, n))
+        for j in (0, 33, 95):
+            o = O.OracleRng(engine, seed=[7], spawn_key=(4, 5 + j))
+            assert np.array_equal(_bits(out[j]), _bits(o.fill(dist, params, n))), (dist, j)
 
 
 def test_streams_continuous():

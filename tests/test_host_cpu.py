@@ -41,10 +41,9 @@ def test_catalogue_and_registry():
     assert engines.normalize(None) == engines.normalize("0") == engines.normalize("") == "x256++simd"
     with pytest.raises(engines.UnknownEngineError):
         engines.normalize("nope")
-    for e in ("x256**", "x256++", "pcg64", "philox", "sfc64", "ranlux++", "x256++simd", "x256**simd", "sfc64simd"):
+    for e in engines.ENGINE_IDS:  # every registry engine has a device path
         assert engines.supported(e)
-    with pytest.raises(NotImplementedError):
-        engines.make("chacha20")
+        assert engines.make(e).ID == e
 
 
 def test_engine_kats_host(golden):
@@ -90,7 +89,7 @@ def test_jumps_and_advance(golden):
 
 
 @pytest.mark.parametrize("engine", ["x256**", "x256++", "pcg64", "philox", "sfc64", "ranlux++", "x256++simd",
-                                    "x256**simd", "sfc64simd"])
+                                    "x256**simd", "sfc64simd", "x128+", "xoro++", "squares", "cwg128", "chacha20"])
 def test_scalar_draws_match_oracle(engine):
     r = state_io.create(engine, seed=[4242])
     o = O.OracleRng(engine, seed=[4242])
@@ -104,6 +103,25 @@ def test_scalar_draws_match_oracle(engine):
     assert a == b
     assert [r.u01f() for _ in range(301)] == [float(x) for x in o.fill("u01f", {}, 301)]
     assert r.get_state() == o.get_state()
+
+
+def test_set_stream_matches_reference(golden):
+    for c in golden["streams"]:
+        r = state_io.create(c["engine"], seed=[88])
+        r.next_u32()
+        r.set_stream(_h(c["words"]))
+        assert r.get_state() == _h(c["state"]), c["engine"]
+        assert [r.next_u64() for _ in range(20)] == _h(c["next"]), c["engine"]
+
+
+def test_chacha20_exhaustion():
+    """counter.py:209-216: generating past block 2^32 - 1 raises OverflowError."""
+    r = state_io.create("chacha20", seed=[5])
+    st = r.get_state()
+    st[5] = (st[5] & 0xFFFFFFFF) | ((2 ** 32 - 2) << 32)
+    r.set_state(st)
+    with pytest.raises(OverflowError):
+        r.next_u64()  # a refill needs 18 blocks, only 2 remain
 
 
 def test_raw_bytes_and_set_stream():

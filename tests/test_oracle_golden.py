@@ -72,6 +72,8 @@ def test_jumped_states(golden):
             st = O.x256_apply_poly(st, O.x_pow2k_mod(j["k"], p))
         elif j["engine"] == "pcg64":
             st = O.pcg_advance(st, 1 << j["k"])
+        elif j["engine"] in ("x128+", "xoro++"):
+            st = O.x128_jump(j["engine"], st, j["k"])
         else:
             st = O.ranlux_jump(st, j["k"])
         assert st == _h(j["state"]), j
