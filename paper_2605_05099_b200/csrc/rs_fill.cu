@@ -133,19 +133,31 @@ template <> struct EngOf<RS_ENG_CWG128> { typedef EngCwg type; };
 // both parse passes read them back instead of regenerating them.
 constexpr int RS_ENG_MEM = 100;
 __device__ u32 g_mem_overrun;
-struct EngMem {  // reads its (per-lane sequential) words 32 bytes at a time
+struct EngMem {  // reads its (per-lane sequential) words 32 bytes at a time, one group ahead
     const u64 *w;
-    u64 idx, nw;
-    u64 b0, b1, b2, b3;
-    int have;
+    u64 idx, nw;   // idx: next word to return
+    u64 g;         // word index of the prefetched group n0..n3
+    u64 b0, b1, b2, b3, n0, n1, n2, n3;
+    int have;      // words left in b (-1: nothing loaded yet)
+    __device__ __forceinline__ void load(u64 at, u64 &x0, u64 &x1, u64 &x2, u64 &x3) {
+        if (at >= nw) { g_mem_overrun = 1; x0 = x1 = x2 = x3 = 0; return; }
+        asm volatile("ld.global.nc.v4.b64 {%0, %1, %2, %3}, [%4];"
+                     : "=l"(x0), "=l"(x1), "=l"(x2), "=l"(x3) : "l"(w + at));
+    }
     __device__ __forceinline__ u64 next() {
-        if (have == 0) {
-            u64 g = idx & ~3ULL;
-            if (g >= nw) { g_mem_overrun = 1; return 0; }
-            asm volatile("ld.global.nc.v4.b64 {%0, %1, %2, %3}, [%4];"
-                         : "=l"(b0), "=l"(b1), "=l"(b2), "=l"(b3) : "l"(w + g));
-            have = 4;
-            for (u64 j = g; j < idx; j++) { b0 = b1; b1 = b2; b2 = b3; have--; }
+        if (have <= 0) {
+            if (have < 0) {  // first use: the group holding idx, then the one after it
+                u64 a = idx & ~3ULL;
+                load(a, b0, b1, b2, b3);
+                have = 4;
+                for (u64 j = a; j < idx; j++) { b0 = b1; b1 = b2; b2 = b3; have--; }
+                g = a + 4;
+            } else {
+                b0 = n0; b1 = n1; b2 = n2; b3 = n3;
+                have = 4;
+                g += 4;
+            }
+            if (g < nw) load(g, n0, n1, n2, n3);
         }
         u64 r = b0;
         b0 = b1; b1 = b2; b2 = b3;
@@ -207,7 +219,7 @@ __device__ __forceinline__ void make_engine(const FillPlan &p, u32 t, typename E
         e.w = p.words;
         e.idx = (u64)t * p.L;
         e.nw = p.nwords;
-        e.have = 0;
+        e.have = -1;
     }
 }
 

@@ -35,7 +35,7 @@ fp = r._continuous_params(a.dist, params, n) if a.dist != "uint64" else []
 fpa = (ctypes.c_double * 4)(*(list(fp) + [0.0] * (4 - len(fp))))
 b = int(params.get("b", 0))
 ipa = _lib.u64_array([b, 0], 4)
-el = 4 if a.dist == "u01f" else 8
+el = 4 if a.dist in ("u01f", "uniff", "normf", "expf") else 8
 out = torch.empty(n * el, dtype=torch.uint8, device="cuda")
 sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(a.reps + 1)]
