@@ -1890,7 +1890,10 @@ rs_status launch_simd(DevCtx &c, FillPlan &p, int mode, cudaStream_t st) {
     const void *fn = simd_kernel(p.engine, mode);
     u64 steps = (p.weng + 7) / 8;
     if (steps == 0) steps = 1;
-    u64 Gfull = (u64)c.sms * occupancy(fn) * BLOCK / 8;  // one wave of lane-threads
+    // an eighth of a wave of lane-threads: the per-lane GF(2) setup (k_x256_setup) costs
+    // per thread, while the store-bound fill saturates HBM well before a full wave
+    // (x256++simd 2^28 normals 3.86 -> 3.71 ms, 2^24 raw 0.28 -> 0.09 ms)
+    u64 Gfull = (u64)c.sms * occupancy(fn) * BLOCK / 64;
     u64 Ls = (steps + Gfull - 1) / Gfull;
     if (Ls < 16) Ls = 16;
     u64 G = (steps + Ls - 1) / Ls;
