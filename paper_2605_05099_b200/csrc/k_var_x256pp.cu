@@ -1,0 +1,20 @@
+// xoshiro256++ parse kernels: k_count / k_fixup / k_emit for every sampler family.
+#include "rs_kernels.cuh"
+
+namespace {
+template <int D>
+rsk::VarKernels vk() {
+    return rsk::VarKernels{(const void *)k_count<RS_ENG_X256PP, D>, (const void *)k_fixup<RS_ENG_X256PP, D>, (const void *)k_emit<RS_ENG_X256PP, D>};
+}
+}  // namespace
+
+rsk::VarKernels rsk::var_kernels_x256pp(int fam) {
+    switch (fam) {
+    case FAM_NORM: return vk<FAM_NORM>();
+    case FAM_EXP: return vk<FAM_EXP>();
+    case FAM_GAMMA: return vk<FAM_GAMMA>();
+    case FAM_F32: return vk<FAM_F32>();
+    case FAM_U32: return vk<FAM_U32>();
+    default: return vk<FAM_LEMIRE>();
+    }
+}

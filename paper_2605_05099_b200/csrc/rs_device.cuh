@@ -431,7 +431,7 @@ RS_DEV u32 hiw(double x) { return (u32)(bits(x) >> 32); }
 RS_DEV double with_hiw(double x, u32 h) { return dbl(((u64)h << 32) | (bits(x) & 0xFFFFFFFFULL)); }
 
 // det_exp, detmath.py:59-104
-__device__ __noinline__ double det_exp_dev(double x) {
+static __device__ __noinline__ double det_exp_dev(double x) {
     const double huge = 1.0e300, twom1000 = 9.33263618503218878990e-302;
     const double o_thr = 7.09782712893383973096e+02, u_thr = -7.45133219101941108420e+02;
     const double invln2 = 1.44269504088896338700e+00, ln2hi = 6.93147180369123816490e-01,
@@ -476,7 +476,7 @@ __device__ __noinline__ double det_exp_dev(double x) {
 }
 
 // det_log, detmath.py:107-163
-__device__ __noinline__ double det_log_dev(double x) {
+static __device__ __noinline__ double det_log_dev(double x) {
     const double ln2hi = 6.93147180369123816490e-01, ln2lo = 1.90821492927058770002e-10;
     const double two54 = 1.80143985094819840000e+16;
     const double Lg1 = 6.666666666666735130e-01, Lg2 = 3.999999999940941908e-01,
