@@ -415,8 +415,29 @@ __device__ __forceinline__ u64 wl_count(const D &d, SRC &s, u64 end, Tally &tl) 
         c += bnd;
     }
     u32 left = s.pos < end ? (u32)(end - s.pos) : 0u, used = 0, cc = 0;
-    // 4 words per step: the engine chain and the 4 strip loads overlap; words generated
-    // past the exit are dropped (only the position matters)
+    // 4 words per step: the engine chain and the 4 strip loads overlap. While a whole
+    // batch lies inside the segment no exit is possible, so the bulk loop tests nothing
+    // per word; the tail loop below stops at the first boundary past the end (words
+    // generated past the exit are dropped: only the position matters).
+    if (bnd) {
+        u32 b = 1;
+        while (used + 4 <= left) {
+            u64 w[4];
+            ZigFast f[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) w[k] = s.e.next();
+#pragma unroll
+            for (int k = 0; k < 4; k++) f[k] = d.strip(w[k]);
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                double z;
+                b = d.feed(m, w[k], f[k], tl, z) ? 1u : 0u;
+                cc += b;
+            }
+            used += 4;
+        }
+        bnd = b != 0;
+    }
     while (!(bnd && used >= left)) {
         u64 w[4];
         ZigFast f[4];
