@@ -467,10 +467,19 @@ __device__ __forceinline__ void wl_emit(const D &d, SRC &s, u64 kmax, W &wr, Tal
         if (d.feed(m, s.next(), tl, z)) { wr.put(d.finish(z)); k++; }
     }
     u32 left = (u32)(kmax - k), used = 0;
+    // one word of software pipelining: the next word is generated and its strip load
+    // issued before the current word is fed (the extra word at the end is never fed;
+    // the position counts fed words only)
+    u64 wn = s.e.next();
+    ZigFast fn = d.strip(wn);
     while (left) {
+        u64 w = wn;
+        ZigFast f = fn;
+        wn = s.e.next();
+        fn = d.strip(wn);
         double z;
         used++;
-        if (d.feed(m, s.e.next(), tl, z)) { wr.put(d.finish(z)); left--; }
+        if (d.feed(m, w, f, tl, z)) { wr.put(d.finish(z)); left--; }
     }
     s.pos += used;
 }
