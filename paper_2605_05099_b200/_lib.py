@@ -6,10 +6,11 @@ loaded, importing the package raises. Build it with `make -C paper_2605_05099_b2
 """
 
 import ctypes
+import os
 import pathlib
 
 HERE = pathlib.Path(__file__).resolve().parent
-LIB_PATH = HERE / "librandstream_b200.so"
+LIB_PATH = pathlib.Path(os.environ.get("RANDSTREAM_B200_LIB", HERE / "librandstream_b200.so"))  # override: A/B builds
 
 CAP = 144
 

@@ -27,10 +27,67 @@ RS_DEV u64 rotl64(u64 x, int k) { return (x << k) | (x >> (64 - k)); }
 
 // ----------------------------------------------------------------------------- engines
 
+// 32-bit halves of a 64-bit register, and funnel-shift rotates (one SHF per half)
+RS_DEV void split64(u64 x, u32 &lo, u32 &hi) { asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(x)); }
+RS_DEV u64 join64(u32 lo, u32 hi) {
+    u64 x;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "r"(lo), "r"(hi));
+    return x;
+}
+RS_DEV u32 shfl_l(u32 a, u32 b, int k) {  // high word of (b:a) << k
+    u32 r;
+    asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(k));
+    return r;
+}
+// x * c for a small constant c on the FMA pipe: IMAD.WIDE.U32 + IMAD (ptxas turns a
+// C-level x*5 into three wide multiplies, or into LEAs that load the ALU pipe)
+RS_DEV void mulc_fma(u32 lo, u32 hi, u32 c, u32 &rlo, u32 &rhi) {
+    asm("{\n\t.reg .u64 w;\n\t.reg .u32 wl, wh;\n\t"
+        "mul.wide.u32 w, %2, %4;\n\tmov.b64 {wl, wh}, w;\n\t"
+        "mad.lo.u32 %1, %3, %4, wh;\n\tmov.b32 %0, wl;\n\t}"
+        : "=r"(rlo), "=r"(rhi) : "r"(lo), "r"(hi), "r"(c));
+}
+
 template <bool SS>
 struct EngX256 {  // xorfam.py:88-124
     u64 s0, s1, s2, s3;
     RS_DEV void load(const u64 *p) { s0 = p[0]; s1 = p[1]; s2 = p[2]; s3 = p[3]; }
+#ifndef RS_X256_C
+    // Per 32-bit halves, so the step costs 13 ALU instructions (8 LOP3, 5 SHF) and
+    // the multiplies (x256**) or adds (x256++) go to the FMA pipe: the two pipes
+    // each take one warp instruction per 2 cycles, and the C form put ~20 on ALU.
+    RS_DEV u64 next() {
+        u32 a0, b0, a1, b1, a2, b2, a3, b3;
+        split64(s0, a0, b0);
+        split64(s1, a1, b1);
+        split64(s2, a2, b2);
+        split64(s3, a3, b3);
+        u32 rl, rh;
+        if (SS) {  // rotl(s1 * 5, 7) * 9
+            u32 ml, mh;
+            mulc_fma(a1, b1, 5u, ml, mh);
+            u32 ql = shfl_l(mh, ml, 7), qh = shfl_l(ml, mh, 7);
+            mulc_fma(ql, qh, 9u, rl, rh);
+        } else {   // rotl(s0 + s3, 23) + s0
+            u64 p = s0 + s3;
+            u32 pl, ph;
+            split64(p, pl, ph);
+            u32 ql = shfl_l(ph, pl, 23), qh = shfl_l(pl, ph, 23);
+            split64(join64(ql, qh) + s0, rl, rh);
+        }
+        u32 tl = a1 << 17, th = shfl_l(a1, b1, 17);           // t = s1 << 17
+        u32 n2l = a2 ^ a0 ^ tl, n2h = b2 ^ b0 ^ th;           // s2 ^= s0; ... s2 ^= t
+        u32 n1l = a1 ^ a2 ^ a0, n1h = b1 ^ b2 ^ b0;           // s1 ^= s2 (new s2 without t)
+        u32 x3l = a3 ^ a1, x3h = b3 ^ b1;                     // s3 ^= s1
+        u32 n0l = a0 ^ x3l, n0h = b0 ^ x3h;                   // s0 ^= s3
+        u32 n3l = shfl_l(x3l, x3h, 45 - 32), n3h = shfl_l(x3h, x3l, 45 - 32);  // rotl(s3, 45)
+        s0 = join64(n0l, n0h);
+        s1 = join64(n1l, n1h);
+        s2 = join64(n2l, n2h);
+        s3 = join64(n3l, n3h);
+        return join64(rl, rh);
+    }
+#else
     RS_DEV u64 next() {
         u64 r = SS ? rotl64(s1 * 5ULL, 7) * 9ULL : rotl64(s0 + s3, 23) + s0;
         u64 t = s1 << 17;
@@ -38,6 +95,7 @@ struct EngX256 {  // xorfam.py:88-124
         s3 = rotl64(s3, 45);
         return r;
     }
+#endif
 };
 
 #define RS_PCG_MULT 0xDA942042E4DD58B5ULL
