@@ -166,16 +166,22 @@ rs_status x256_mats(DevCtx &c, int engine, u64 L, int levels, u64 **out) {
     return RS_OK;
 }
 
-int occupancy(const void *fn) {
-    static std::map<const void *, int> cache;
-    auto it = cache.find(fn);
+// resident blocks per SM; a kernel with dynamic shared memory gets its opt-in limit set
+// here first (per device), so call this before launching it
+int occupancy(const void *fn, size_t smem = 0) {
+    static std::map<std::tuple<int, const void *, size_t>, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto key = std::make_tuple(dev, fn, smem);
+    auto it = cache.find(key);
     if (it != cache.end()) return it->second;
+    if (smem > 0) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BLOCK, 0) != cudaSuccess || nb < 1) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BLOCK, smem) != cudaSuccess || nb < 1) {
         cudaGetLastError();
         nb = 1;
     }
-    cache[fn] = nb;
+    cache[key] = nb;
     return nb;
 }
 
@@ -220,8 +226,8 @@ using rsk::philox_kernel;
 using rsk::serial_kernel;
 using rsk::simd_kernel;
 
-rs_status launch(const void *fn, dim3 g, dim3 b, void **args, cudaStream_t st) {
-    CK(cudaLaunchKernel(fn, g, b, args, 0, st));
+rs_status launch(const void *fn, dim3 g, dim3 b, void **args, cudaStream_t st, size_t smem = 0) {
+    CK(cudaLaunchKernel(fn, g, b, args, smem, st));
     return RS_OK;
 }
 
@@ -593,9 +599,9 @@ rs_status launch_raw_words(DevCtx &c, FillPlan &m, cudaStream_t st) {
         return launch(fn, dim3((unsigned)g), dim3(BLOCK), args, st);
     }
     const void *fn = fixed_kernel(m.engine, FX_RAW);
-    if ((rc = plan_segments(c, m, m.weng, 64, occupancy(fn), st, true, 144))) return rc;
+    if ((rc = plan_segments(c, m, m.weng, 64, occupancy(fn, FX_SMEM), st, true, 144))) return rc;
     void *args[] = {&m};
-    return launch(fn, dim3(m.T / BLOCK), dim3(BLOCK), args, st);
+    return launch(fn, dim3(m.T / BLOCK), dim3(BLOCK), args, st, FX_SMEM);
 }
 
 // The device part of one fill. On return (sync=true) `E` holds the stream units
@@ -674,10 +680,10 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
             return RS_OK;
         }
         const void *fn = fixed_kernel(s->engine, r.fixed_mode);
-        rc = plan_segments(c, p, p.weng ? p.weng : 1, 64, occupancy(fn), st, true, 144);
+        rc = plan_segments(c, p, p.weng ? p.weng : 1, 64, occupancy(fn, FX_SMEM), st, true, 144);
         if (rc) return rc;
         void *args[] = {&p};
-        rc = launch(fn, dim3(p.T / BLOCK), dim3(BLOCK), args, st);
+        rc = launch(fn, dim3(p.T / BLOCK), dim3(BLOCK), args, st, FX_SMEM);
         if (rc) return rc;
         E = n;
         chunks = 1;
