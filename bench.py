@@ -331,19 +331,19 @@ def run_per_config(dev, stream, sptr, buf, peak):
     time_fill("extra_ranlux_raw_2p28", "ranlux++", [12345], "uint64", {}, 1 << 28, reps=2)
     # C5b: sfc64 per-stream Lemire, 2^16 streams x 4096
     for m in (6, 1000003, (1 << 63) + 1):
-        fill_streams("sfc64", [31], [], 0, 1 << 16, "uint64", {"b": m}, 4096)
+        rows = fill_streams("sfc64", [31], [], 0, 1 << 16, "uint64", {"b": m}, 4096)
         torch.cuda.synchronize()
         a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(3):
-            fill_streams("sfc64", [31], [], 0, 1 << 16, "uint64", {"b": m}, 4096)
+            fill_streams("sfc64", [31], [], 0, 1 << 16, "uint64", {"b": m}, 4096, out=rows)
         z.record(stream)
         torch.cuda.synchronize()
         ms = a.elapsed_time(z) / 3
         n = 1 << 28
         res["c5b_sfc64_streams_lemire_%d_2p28" % m] = {"gsamples_s": n / (ms / 1e3) / 1e9, "ms": ms, "n": n,
                                                        "hbm_frac": n * 8 / (ms / 1e3) / 1e9 / peak,
-                                                       "note": "includes a 2 GiB output allocation per call"}
+                                                       "note": "fill_streams(..., out=) into a resident 2 GiB tensor"}
     # C5a: mvn (z fill + cuBLAS DGEMM), d in {64, 256, 512}, n = 2^20
     for d in (64, 256, 512):
         r = state_io.create("philox", seed=[31])

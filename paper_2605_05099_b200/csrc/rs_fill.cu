@@ -1013,8 +1013,8 @@ rs_status rs_fill_streams(int32_t engine, const uint64_t *seed, int32_t n_seed, 
     }
     const void *fn = rsk::streams_kernel(engine, d);
     void *args[] = {&a};
-    unsigned g2 = (unsigned)((n_streams + BLOCK - 1) / BLOCK);
-    if ((rc = launch(fn, dim3(g2), dim3(BLOCK), args, st))) return rc;
+    unsigned g2 = (unsigned)((n_streams + STR_BLOCK - 1) / STR_BLOCK);
+    if ((rc = launch(fn, dim3(g2), dim3(STR_BLOCK), args, st, ST_SMEM))) return rc;
     if (sg.host) {
         CK(cudaMemcpyAsync(out, sg.dptr, bytes, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
@@ -1082,24 +1082,51 @@ rs_status rs_mvn(rs_stream *s, const double *L, const double *mean, int64_t d, u
     } else {
         X = out;
     }
-    {
-        u64 nn = n;
-        void *ia[] = {&X, &md, &d, &nn, &layout};
-        rs_status irc = launch(rsk::mvn_init_kernel(), dim3((unsigned)std::min<u64>((nz + 255) / 256, 148 * 16)),
-                               dim3(256), ia, st);
-        if (irc) return irc;
-    }
+    u64 nn = n;
+    const unsigned ig = (unsigned)std::min<u64>((nz + 255) / 256, 148 * 16);
     cublasSetStream(c->blas, st);
     double one = 1.0;
     cublasStatus_t bs;
-    if (layout == 0) {
-        // X (n x d row-major) = (d x n col-major) C = L * z^T : A = L buffer (row-major => col-major L^T), op T
-        bs = cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)d, (int)n, (int)d, &one, Ld, (int)d, z, (int)d, &one,
-                         X, (int)d);
+    // a Cholesky factor is lower triangular; the pivoted semidefinite factor is not
+    // (continuous.py:293-309), and takes the dense GEMM
+    bool lower = true;
+    {
+        std::vector<double> hl;
+        const double *Lh = L;
+        if (is_device_ptr(L)) {
+            hl.resize((size_t)d * d);
+            CK(cudaMemcpyAsync(hl.data(), L, (size_t)d * d * 8, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            Lh = hl.data();
+        }
+        for (int64_t r = 0; r < d && lower; r++)
+            for (int64_t q = r + 1; q < d; q++)
+                if (Lh[r * d + q] != 0.0) { lower = false; break; }
+    }
+    // (below d ~ 200 the DGEMM is faster than cuBLAS's TRMM on B200: d = 64 1.70 vs 1.82 ms)
+    if (layout == 0 && lower && d >= 192) {
+        // X (n x d row-major) = (d x n col-major) C = L * z^T. L is lower triangular, so a
+        // TRMM does the d(d+1)/2 nonzero products per vector, half the DGEMM's d^2: the
+        // L buffer (row-major L) is col-major L^T, upper, used transposed; B = z^T.
+        bs = cublasDtrmm(c->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)d,
+                         (int)n, &one, Ld, (int)d, z, (int)d, X, (int)d);
+        if (bs != CUBLAS_STATUS_SUCCESS) { rs::set_error("cublasDtrmm failed"); return RS_ERR_CUDA; }
+        int add = 1;
+        void *ia[] = {&X, &md, &d, &nn, &layout, &add};
+        if ((rc = launch(rsk::mvn_init_kernel(), dim3(ig), dim3(256), ia, st))) return rc;
     } else {
-        // X^T (d x n row-major) = (n x d col-major) C = z * L^T : z buffer is (d x n) col-major -> op T
-        bs = cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)n, (int)d, (int)d, &one, z, (int)d, Ld, (int)d, &one,
-                         X, (int)n);
+        int add = 0;
+        void *ia[] = {&X, &md, &d, &nn, &layout, &add};
+        if ((rc = launch(rsk::mvn_init_kernel(), dim3(ig), dim3(256), ia, st))) return rc;
+        if (layout == 0) {
+            // X (n x d row-major) = (d x n col-major) C = L * z^T : A = L buffer (row-major => col-major L^T), op T
+            bs = cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)d, (int)n, (int)d, &one, Ld, (int)d, z, (int)d,
+                             &one, X, (int)d);
+        } else {
+            // X^T (d x n row-major) = (n x d col-major) C = z * L^T : z buffer is (d x n) col-major -> op T
+            bs = cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)n, (int)d, (int)d, &one, z, (int)d, Ld, (int)d,
+                             &one, X, (int)n);
+        }
     }
     if (bs != CUBLAS_STATUS_SUCCESS) { rs::set_error("cublasDgemm failed"); return RS_ERR_CUDA; }
     if (host_out) CK(cudaMemcpyAsync(out, X, nz * 8, cudaMemcpyDeviceToHost, st));

@@ -1196,8 +1196,43 @@ __device__ void seed_fe128(const StreamArgs &a, u64 j, u64 *out, int nout) {
     }
 }
 
+// Per-stream rows of 8-byte outputs (row j = [j * nper, (j + 1) * nper), every row the
+// same length): each lane fills 32 outputs of its row into its row of the warp tile,
+// then the warp stores two lanes' 256-byte chunks per STG.128 instruction (the fixed
+// fills' pattern, write_run). produce() returns the lane's next output as bits.
+template <class F>
+__device__ __forceinline__ void stream_rows8(u64 *out, u64 j, u64 nper, bool valid, u64 (*tile)[FX_ROW], F produce) {
+    const u32 lane = threadIdx.x & 31;
+    const u64 nch = nper / FX_CH;
+    const u64 row = (u64)(uintptr_t)(out + j * nper);
+    for (u64 k = 0; k < nch; k++) {
+        if (valid) {
+#pragma unroll 4
+            for (int c = 0; c < FX_CH; c++) tile[lane][c] = produce();
+        }
+        __syncwarp();
+        const u64 dst = valid ? row + k * FX_CH * 8 : 0;
+#pragma unroll
+        for (int g = 0; g < 16; g++) {
+            u32 r = 2 * g + (lane >> 4), c = lane & 15;
+            u64 d = __shfl_sync(0xFFFFFFFFu, dst, r);
+            if (d) {
+                u64 x = tile[r][2 * c], y = tile[r][2 * c + 1];
+                asm volatile("st.global.v2.b64 [%0], {%1, %2};" ::"l"(d + 16 * c), "l"(x), "l"(y) : "memory");
+            }
+        }
+        __syncwarp();
+    }
+    if (valid)
+        for (u64 i = nch * FX_CH; i < nper; i++) out[j * nper + i] = produce();
+}
+
+// 64-thread blocks: one thread per stream cannot be split (sfc64 has no skip-ahead), so
+// small blocks spread the few warps evenly over the SMs (2^16 streams: 13.8 warps/SM)
+constexpr int STR_BLOCK = 64;
+constexpr size_t ST_SMEM = (size_t)(STR_BLOCK / 32) * 32 * FX_ROW * 8;  // dynamic shared memory of k_streams
 template <int E, int D>
-__global__ void __launch_bounds__(BLOCK) k_streams(const __grid_constant__ StreamArgs a) {
+__global__ void __launch_bounds__(STR_BLOCK) k_streams(const __grid_constant__ StreamArgs a) {
     __shared__ ZigFast sm[256];
     if (a.zfast) {
         for (int i = threadIdx.x; i < 256; i += blockDim.x) sm[i] = a.zfast[i];
@@ -1205,10 +1240,19 @@ __global__ void __launch_bounds__(BLOCK) k_streams(const __grid_constant__ Strea
         for (int i = threadIdx.x; i < 256; i += blockDim.x) ((ZigFastF *)sm)[i] = a.zfastf[i];
     }
     __syncthreads();
-    u64 j = (u64)blockIdx.x * BLOCK + threadIdx.x;
-    if (j >= a.nstreams) return;
+    u64 j = (u64)blockIdx.x * STR_BLOCK + threadIdx.x;
+    // 8-byte rows through the warp tile (whole warps: no early exit) when every row
+    // start is 16-byte aligned; otherwise the per-thread writers below
+    extern __shared__ __align__(16) u64 st_dyn[];  // ST_SMEM
+    constexpr bool W8 = sizeof(typename DistOf<D == FAM_FIXED ? FAM_LEMIRE : D>::type::out_t) == 8;
+    const bool tiled = W8 && !(D == FAM_FIXED && is_half(a.fmode)) && a.nper % 2 == 0 &&
+                       (((uintptr_t)a.out) & 15) == 0;
+    if (!tiled && j >= a.nstreams) return;
+    const bool valid = j < a.nstreams;
+    u64 (*tile)[FX_ROW] = (u64 (*)[FX_ROW])(st_dyn + (threadIdx.x >> 5) * 32 * FX_ROW);
     u64 w[9];
     typename EngOf<E>::type e;
+    if (valid) {
     if constexpr (E == RS_ENG_SFC64) {
         seed_fe128(a, a.j0 + j, w, 3);
         e.a = w[0]; e.b = w[1]; e.c = w[2]; e.w = 1;  // sfc.py:53-55
@@ -1245,11 +1289,16 @@ __global__ void __launch_bounds__(BLOCK) k_streams(const __grid_constant__ Strea
         if (!(w[0] | w[1] | w[2] | w[3])) w[0] = 1;
         e.s0 = w[0]; e.s1 = w[1]; e.s2 = w[2]; e.s3 = w[3];
     }
+    }  // valid
     // Per-stream rows go out through VecWriter8 (8-byte) / ScalarWriter (4-byte). The
     // shared-memory RingWriter used by k_emit produced an illegal address here in some
     // configurations (x256**/pcg64 normals, >= 8 streams) that vanished under printf
     // instrumentation; it stays out of this kernel until that is understood.
     if constexpr (D == FAM_FIXED) {  // raw / uniform / masked laws: a fresh stream, no pending half
+        if (tiled) {
+            stream_rows8((u64 *)a.out, j, a.nper, valid, tile, [&]() { return fx_map_rt(a, e.next()); });
+            return;
+        }
         if (is_half(a.fmode)) {  // low half first, a trailing high half dropped
             ScalarWriter<u32> wr;
             wr.init((u32 *)a.out, j * a.nper);
@@ -1272,9 +1321,26 @@ __global__ void __launch_bounds__(BLOCK) k_streams(const __grid_constant__ Strea
     DistArgs da{a.fp, a.ip, &a.ga, &a.gb, a.kind, a.fm, a.zslow, a.zslowf};
     make_dist_a<D == FAM_FIXED ? FAM_LEMIRE : D>(da, sm, d);
     typedef typename DT::out_t T;
+    Tally tl;
+    if constexpr (sizeof(T) == 8) {
+        if (tiled) {
+            if constexpr (D == FAM_LEMIRE) {
+                stream_rows8((u64 *)a.out, j, a.nper, valid, tile, [&]() {
+                    u64 o;
+                    while (!d.accept(e.next(), o)) {}
+                    return o;
+                });
+            } else {  // 8-byte samplers are word-fed
+                stream_rows8((u64 *)a.out, j, a.nper, valid, tile, [&]() {
+                    T v = d.sample(e, tl);
+                    return *(u64 *)&v;
+                });
+            }
+            return;
+        }
+    }
     typename std::conditional<sizeof(T) == 8, VecWriter8<T>, ScalarWriter<T>>::type wr;
     wr.init((T *)a.out, j * a.nper);
-    Tally tl;
     if constexpr (D == FAM_LEMIRE) {
         for (u64 i = 0; i < a.nper;) {
             u64 o;
@@ -1296,13 +1362,16 @@ __global__ void __launch_bounds__(BLOCK) k_streams(const __grid_constant__ Strea
 }
 
 #ifdef RS_KERNELS_MISC
-__global__ void k_mvn_init(double *c, const double *mean, int64_t d, u64 n, int layout) {
+// layout n_d: C is d x n col-major => element i belongs to row i % d
+// layout d_n: C is n x d col-major => element i belongs to column i / n
+// add = 0: C = mean (before a beta = 1 GEMM); add = 1: C = mean + C (after the TRMM),
+// the reference's `mean + z @ factor.T` (continuous.py:331-336)
+__global__ void k_mvn_init(double *c, const double *mean, int64_t d, u64 n, int layout, int add) {
     u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
     u64 tot = n * (u64)d;
     for (; i < tot; i += (u64)gridDim.x * blockDim.x) {
-        // layout n_d: C is d x n col-major => element i belongs to row i % d
-        // layout d_n: C is n x d col-major => element i belongs to column i / n
-        c[i] = layout == 0 ? mean[i % d] : mean[i / n];
+        double m = layout == 0 ? mean[i % d] : mean[i / n];
+        c[i] = add ? m + c[i] : m;
     }
 }
 #endif  // RS_KERNELS_MISC

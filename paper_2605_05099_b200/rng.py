@@ -540,9 +540,11 @@ def semidefinite_factor(cov):
         return m
 
 
-def fill_streams(engine, seed, spawn_prefix, j0, n_streams, dist, params, n_per_stream, device=None):
+def fill_streams(engine, seed, spawn_prefix, j0, n_streams, dist, params, n_per_stream, device=None, out=None):
     """Per-stream mode: row s = create(engine, seed, spawn_key=prefix + (j0 + s,)).fill(dist, params, n)
-    for s < n_streams, computed by one GPU thread per stream (sfc64's parallel form)."""
+    for s < n_streams, computed by one GPU thread per stream (sfc64's parallel form).
+    `out`: an optional contiguous CUDA tensor of shape (n_streams, n_per_stream) and the
+    law's dtype to fill in place (returned)."""
     eid = engines.normalize(engine)
     params = dict(params or {})
     n_streams, n_per_stream = int(n_streams), int(n_per_stream)
@@ -551,8 +553,15 @@ def fill_streams(engine, seed, spawn_prefix, j0, n_streams, dist, params, n_per_
         fp, ip = [0.0] * 4, probe._discrete_params(dist, params, 1)
     else:
         fp, ip = probe._continuous_params(dist, params, 1), [0, 0, 0, 0]
-    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-    out = torch.empty((n_streams, n_per_stream), dtype=_out_dtype(dist), device=dev)
+    if out is not None:
+        if (not out.is_cuda or not out.is_contiguous() or tuple(out.shape) != (n_streams, n_per_stream)
+                or out.dtype != _out_dtype(dist)):
+            raise ValueError("out must be a contiguous CUDA tensor of shape (n_streams, n_per_stream) and dtype %s"
+                             % _out_dtype(dist))
+        dev = out.device
+    else:
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        out = torch.empty((n_streams, n_per_stream), dtype=_out_dtype(dist), device=dev)
     seedw = [int(w) & MASK64 for w in seed]
     pre = [int(w) & MASK64 for w in spawn_prefix]
     _lib.check(_lib.lib.rs_fill_streams(engines.NATIVE_ID[eid], _lib.u64_array(seedw), len(seedw),

@@ -245,6 +245,22 @@ def test_streams_every_engine(engine):
             assert np.array_equal(_bits(out[j]), _bits(o.fill(dist, params, n))), (dist, j)
 
 
+@pytest.mark.parametrize("engine", ["sfc64", "pcg64", "x256**"])
+def test_streams_tiled_rows(engine):
+    """8-byte rows through the warp tile (even row length): partial warps (45 streams),
+    rows that are not whole 32-sample chunks, and the caller's out= tensor."""
+    for dist, params, n in (("uint64", {}, 1002), ("u01", {}, 64), ("norm", {}, 994), ("uint64", {"b": 10}, 130),
+                            ("exp", {}, 2)):
+        out = fill_streams(engine, [11], [], 2, 45, dist, params, n)
+        again = torch.empty_like(out)
+        assert fill_streams(engine, [11], [], 2, 45, dist, params, n, out=again) is again
+        assert torch.equal(out, again)
+        host = _np(out)
+        for j in (0, 31, 32, 44):
+            o = O.OracleRng(engine, seed=[11], spawn_key=(2 + j,))
+            assert np.array_equal(_bits(host[j]), _bits(o.fill(dist, params, n))), (dist, j)
+
+
 def test_streams_continuous():
     out = _np(fill_streams("sfc64", [5], [2], 10, 300, "norm", {}, 777))
     for j in (0, 299):
@@ -276,6 +292,29 @@ def test_mvn(golden_arrays, d, n, layout):
         X0 = _np(r0.mvn(np.zeros(d), A0 @ A0.T / d + np.eye(d), n=n))
         ref0 = golden_arrays["mvn_X"]
         assert np.max(np.abs(X0 - ref0)) <= 1e-12 * np.max(np.abs(ref0))
+
+
+@pytest.mark.parametrize("layout", ["n_d", "d_n"])
+def test_mvn_semidefinite(layout):
+    """rank-deficient covariance: the pivoted (non-triangular) factor of continuous.py:293-309
+    takes the dense GEMM; the Cholesky one the triangular product (TRMM)."""
+    from paper_2605_05099_b200.rng import semidefinite_factor
+    d, n = 24, 2048
+    B = np.random.default_rng(3).standard_normal((d, 5))
+    S = B @ B.T
+    Lf = semidefinite_factor(S)
+    assert np.any(np.triu(Lf, 1) != 0.0)  # not triangular
+    r = state_io.create("pcg64", seed=[8])
+    o = O.OracleRng("pcg64", seed=[8])
+    mean = np.arange(d, dtype=np.float64)
+    X = _np(r.mvn(mean, S, n=n, layout=layout))
+    z = o.fill("stdnorm", {}, n * d).reshape(n, d)
+    ref = mean + z @ Lf.T
+    if layout == "d_n":
+        X = X.T
+    scale = np.abs(z) @ np.abs(Lf).T + np.abs(mean)
+    assert np.max(np.abs(X - ref) / scale) <= 1e-12
+    _assert_same_position(r, o)
 
 
 def test_tallies_resample_rate():
