@@ -1156,6 +1156,57 @@ struct RingWriter {
     }
 };
 
+// RingWriter with the flush taken off the per-sample path: a ring of two 32-byte groups
+// per thread, and tick() -- called by every lane of a warp on the same steps, once per G
+// steps of a word-level loop that emits at most one sample per step -- stores at most one
+// complete group. A lane's groups then leave on the same steps as its neighbours'
+// instead of a divergent flush on nearly every step (some lane of 32 is always at its
+// group end). Buffered samples stay below 2G: <= G-1 after a tick, + G before the next.
+template <class T, int NT>
+struct BatchRing {
+    static constexpr int G = 32 / (int)sizeof(T);
+    T *abase;  // 32-byte aligned base
+    u64 pos;   // element index (from abase) of the next sample
+    u64 fl;    // first element not yet stored
+    T *ring;   // this thread's slot 0; slot k at ring[k * NT]
+    RS_DEV void init(T *out, u64 start, T *ring_) {
+        ring = ring_;
+        uintptr_t a = (uintptr_t)out;
+        abase = (T *)(a & ~(uintptr_t)31);
+        pos = fl = start + (u64)((a & 31) / sizeof(T));
+    }
+    RS_DEV void put(T v) {
+        ring[(int)(pos & (2 * G - 1)) * NT] = v;
+        pos++;
+    }
+    RS_DEV void tick() {
+        u64 g0 = fl & ~(u64)(G - 1);
+        if (pos < g0 + G) return;
+        T *p = abase + g0;
+        int b = (int)(g0 & (2 * G - 1));  // ring slot of the group's first element
+        if (fl == g0) {
+            u64 q[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                if constexpr (sizeof(T) == 8) {
+                    q[k] = *(const u64 *)&ring[(b + k) * NT];
+                } else {
+                    u64 lo = *(const u32 *)&ring[(b + 2 * k) * NT], hi = *(const u32 *)&ring[(b + 2 * k + 1) * NT];
+                    q[k] = lo | (hi << 32);
+                }
+            }
+            asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(q[0]), "l"(q[1]), "l"(q[2]),
+                         "l"(q[3]) : "memory");
+        } else {  // the run's first group is shared with the previous run
+            for (int k = (int)(fl - g0); k < G; k++) p[k] = ring[(b + k) * NT];
+        }
+        fl = g0 + G;
+    }
+    RS_DEV void finish() {
+        for (u64 a = fl; a < pos; a++) abase[a] = ring[(int)(a & (2 * G - 1)) * NT];
+    }
+};
+
 template <class T>
 struct ScalarWriter {
     T *ptr;

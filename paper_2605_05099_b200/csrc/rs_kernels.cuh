@@ -465,6 +465,7 @@ __device__ __forceinline__ void wl_emit(const D &d, SRC &s, u64 kmax, W &wr, Tal
     while (s.npre > 0 && k < kmax) {
         double z;
         if (d.feed(m, s.next(), tl, z)) { wr.put(d.finish(z)); k++; }
+        wr.tick();  // (thread 0 only: one sample per tick keeps the ring bound)
     }
     u32 left = (u32)(kmax - k), used = 0;
     // one word of software pipelining: the next word is generated and its strip load
@@ -480,6 +481,7 @@ __device__ __forceinline__ void wl_emit(const D &d, SRC &s, u64 kmax, W &wr, Tal
         double z;
         used++;
         if (d.feed(m, w, f, tl, z)) { wr.put(d.finish(z)); left--; }
+        if ((used & (W::G - 1)) == 0) wr.tick();  // the same steps in every lane of the warp
     }
     s.pos += used;
 }
@@ -710,7 +712,7 @@ template <int E, int D>
 __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constant__ FillPlan p, const u32 *entry, const u64 *cnt,
                                                 const u64 *off, const u32 *ex, DevResult *res) {
     __shared__ ZigFast sm[256];
-    __shared__ __align__(16) unsigned char ring_sm[32 * BLOCK];
+    __shared__ __align__(16) unsigned char ring_sm[64 * BLOCK];  // RingWriter: 32 B, BatchRing: 64 B per thread
     stage_tables(p, sm);
     u32 t = blockIdx.x * BLOCK + threadIdx.x;
     Tally tl = {0, 0, 0, 0, 0};
@@ -727,28 +729,38 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constan
             typename DistOf<D>::type d;
             make_dist<D>(p, sm, d);
             typedef typename DistOf<D>::type::out_t T;
-            RingWriter<T, BLOCK> wr;
-            wr.init((T *)p.out, p.out0 + o, (T *)ring_sm + threadIdx.x);
-            if constexpr (D == FAM_LEMIRE || D == FAM_U32) {
+            T *ring = (T *)ring_sm + threadIdx.x;
+            if constexpr (D == FAM_LEMIRE || D == FAM_U32) {  // one unit per step, <= 1 sample
+                BatchRing<T, BLOCK> wr;
+                wr.init((T *)p.out, p.out0 + o, ring);
+                u32 it = 0;
                 for (u64 k = 0; k < kmax;) {
                     T v;
                     bool ok;
                     if constexpr (D == FAM_LEMIRE) ok = d.accept(s.next(), v);
                     else ok = d.accept(s.next32(), v);
                     if (ok) { wr.put(v); k++; }
+                    if ((++it & (BatchRing<T, BLOCK>::G - 1)) == 0) wr.tick();
                 }
+                wr.finish();
             } else {
                 bool done = false;
                 if constexpr (D == FAM_NORM || D == FAM_EXP) {
                     if (d.word_level()) {
+                        BatchRing<T, BLOCK> wr;
+                        wr.init((T *)p.out, p.out0 + o, ring);
                         wl_emit(d, s, kmax, wr, tl);
+                        wr.finish();
                         done = true;
                     }
                 }
-                if (!done)
+                if (!done) {  // sample-level: lanes out of step, flush when a group is full
+                    RingWriter<T, BLOCK> wr;
+                    wr.init((T *)p.out, p.out0 + o, ring);
                     for (u64 k = 0; k < kmax; k++) wr.put(d.sample(s, tl));
+                    wr.finish();
+                }
             }
-            wr.finish();
             if (o + kmax == p.n) res->end_pos = s.pos;
         }
     }
@@ -805,17 +817,22 @@ __device__ __forceinline__ u64 fx_map(const PL &p, u64 w) {
 // out[i] = map(word i) for i in [first, last). Each lane owns a contiguous run,
 // so direct stores from a warp would touch 32 different lines. Instead lanes
 // write 32-word chunks (256 bytes, two lines) into a padded per-warp shared tile
-// (row stride 33 words: conflict-free), and each STG.128 instruction of the warp
+// (fx_at), and each STG.128 instruction of the warp
 // then stores two lanes' chunks, 256 contiguous bytes per half-warp. Measured on
 // B200 for 8 GiB of per-lane runs: 5.8 TB/s with 256-byte runs per instruction vs
 // 4.6 TB/s with 128-byte ones (exp/wpeak2.cu). The ragged head (up to line
 // alignment, and the buffered prefix) and tail are scalar.
 constexpr int FX_CH = 32;
+// Row stride 33 words: the lanes' row-wise STS.64 are conflict-free and the store
+// phase's LDS.64 pairs 2-way conflicted. An XOR-swizzled unpadded layout (conflict-free
+// LDS.128) measured slower -- 1.80 vs 1.51 ms for x256** 2^30 -- because its per-word
+// address arithmetic lands on the ALU pipe, which the xoshiro step already fills (74 %).
 constexpr int FX_ROW = FX_CH + 1;
 constexpr size_t FX_SMEM = (size_t)(BLOCK / 32) * 32 * FX_ROW * 8;  // dynamic shared memory of k_fixed
+__device__ __forceinline__ u32 fx_at(u32 l, u32 j) { return l * FX_ROW + j; }
 template <int E, int MODE>
 __device__ __forceinline__ void write_run(const FillPlan &p, Src<E> &s, u64 *out, u64 first, u64 last,
-                                          u64 (*tile)[FX_ROW], bool active) {
+                                          u64 *tile, bool active) {
     const u32 lane = threadIdx.x & 31;
     u64 i = first;
     if (active)
@@ -832,10 +849,10 @@ __device__ __forceinline__ void write_run(const FillPlan &p, Src<E> &s, u64 *out
         if (has) {
             if constexpr (E == RS_ENG_RANLUX) {  // keep the 9x9-limb mulmod out of an unrolled body (I-cache)
 #pragma unroll 1
-                for (int j = 0; j < FX_CH; j++) tile[lane][j] = fx_map<MODE>(p, s.e.next());
+                for (int j = 0; j < FX_CH; j++) tile[fx_at(lane, j)] = fx_map<MODE>(p, s.e.next());
             } else {
 #pragma unroll
-                for (int j = 0; j < FX_CH; j++) tile[lane][j] = fx_map<MODE>(p, s.e.next());
+                for (int j = 0; j < FX_CH; j++) tile[fx_at(lane, j)] = fx_map<MODE>(p, s.e.next());
             }
         }
         u64 dst = has ? (u64)(uintptr_t)(out + i) : 0;
@@ -845,7 +862,7 @@ __device__ __forceinline__ void write_run(const FillPlan &p, Src<E> &s, u64 *out
             u32 r = 2 * g + (lane >> 4), c = lane & 15;
             u64 d = __shfl_sync(0xFFFFFFFFu, dst, r);
             if (d) {
-                u64 x = tile[r][2 * c], y = tile[r][2 * c + 1];
+                u64 x = tile[fx_at(r, 2 * c)], y = tile[fx_at(r, 2 * c + 1)];
                 asm volatile("st.global.v2.b64 [%0], {%1, %2};" ::"l"(d + 16 * c), "l"(x), "l"(y) : "memory");
             }
         }
@@ -859,7 +876,7 @@ __device__ __forceinline__ void write_run(const FillPlan &p, Src<E> &s, u64 *out
 template <int E, int MODE>
 __global__ void __launch_bounds__(BLOCK) k_fixed(const __grid_constant__ FillPlan p) {
     extern __shared__ __align__(16) u64 fx_dyn[];  // FX_SMEM
-    u64 (*tile)[FX_ROW] = (u64 (*)[FX_ROW])(fx_dyn + (threadIdx.x >> 5) * 32 * FX_ROW);
+    u64 *tile = fx_dyn + (threadIdx.x >> 5) * 32 * FX_ROW;
     u32 t = blockIdx.x * BLOCK + threadIdx.x;
     // every lane of a warp takes part in the tile stores; idle lanes just contribute nothing
     bool active = t < p.T && ((u64)t * p.L < p.weng || t == 0);
@@ -1201,14 +1218,14 @@ __device__ void seed_fe128(const StreamArgs &a, u64 j, u64 *out, int nout) {
 // then the warp stores two lanes' 256-byte chunks per STG.128 instruction (the fixed
 // fills' pattern, write_run). produce() returns the lane's next output as bits.
 template <class F>
-__device__ __forceinline__ void stream_rows8(u64 *out, u64 j, u64 nper, bool valid, u64 (*tile)[FX_ROW], F produce) {
+__device__ __forceinline__ void stream_rows8(u64 *out, u64 j, u64 nper, bool valid, u64 *tile, F produce) {
     const u32 lane = threadIdx.x & 31;
     const u64 nch = nper / FX_CH;
     const u64 row = (u64)(uintptr_t)(out + j * nper);
     for (u64 k = 0; k < nch; k++) {
         if (valid) {
 #pragma unroll 4
-            for (int c = 0; c < FX_CH; c++) tile[lane][c] = produce();
+            for (int c = 0; c < FX_CH; c++) tile[fx_at(lane, c)] = produce();
         }
         __syncwarp();
         const u64 dst = valid ? row + k * FX_CH * 8 : 0;
@@ -1217,7 +1234,7 @@ __device__ __forceinline__ void stream_rows8(u64 *out, u64 j, u64 nper, bool val
             u32 r = 2 * g + (lane >> 4), c = lane & 15;
             u64 d = __shfl_sync(0xFFFFFFFFu, dst, r);
             if (d) {
-                u64 x = tile[r][2 * c], y = tile[r][2 * c + 1];
+                u64 x = tile[fx_at(r, 2 * c)], y = tile[fx_at(r, 2 * c + 1)];
                 asm volatile("st.global.v2.b64 [%0], {%1, %2};" ::"l"(d + 16 * c), "l"(x), "l"(y) : "memory");
             }
         }
@@ -1249,7 +1266,7 @@ __global__ void __launch_bounds__(STR_BLOCK) k_streams(const __grid_constant__ S
                        (((uintptr_t)a.out) & 15) == 0;
     if (!tiled && j >= a.nstreams) return;
     const bool valid = j < a.nstreams;
-    u64 (*tile)[FX_ROW] = (u64 (*)[FX_ROW])(st_dyn + (threadIdx.x >> 5) * 32 * FX_ROW);
+    u64 *tile = st_dyn + (threadIdx.x >> 5) * 32 * FX_ROW;
     u64 w[9];
     typename EngOf<E>::type e;
     if (valid) {
