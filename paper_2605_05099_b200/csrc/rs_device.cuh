@@ -972,6 +972,29 @@ struct DistExp {  // continuous.py:165-169 (exp), :252-254 (pareto), :257-266 (g
         return a > 0.0 ? b + c * (p - 1.0) / a : b - c * (1.0 - 1.0 / p) / a;
     }
 };
+// ----------------------------------------------------------------------------- attempt-level gamma
+// The attempt's first two words, drawn by the caller, then the stream: the source of the
+// exact normal draw(s) when the first word is not a fast-path token or t <= 0 (an
+// attempt always consumes both: a normal token >= 1 word, then the uniform).
+template <class S>
+struct PairSrc {
+    u64 w1, w2;
+    int k;
+    S *s;
+    RS_DEV u64 next() {
+        if (k == 0) { k = 1; return w1; }
+        if (k == 1) { k = 2; return w2; }
+        return s->next();
+    }
+};
+// Per-lane state of the attempt-level machine: which sub-sample is being drawn (beta / f
+// draw x from ga then y from gb, continuous.py:215-218, :237-243), the finished x, and
+// whether the parse started with a lone second sub-sample (the phase-1 parse).
+struct GammaAM {
+    u32 role, lone;
+    double x;
+};
+
 enum { GK_GAMMA = 0, GK_BETA = 1, GK_T = 2, GK_F = 3 };
 struct DistGamma {  // continuous.py:183-212 (gamma, chi2 = gamma(nu/2, 2)), :215-218 beta, :228-234 t, :237-243 f
     typedef double out_t;
@@ -985,6 +1008,65 @@ struct DistGamma {  // continuous.py:183-212 (gamma, chi2 = gamma(nu/2, 2)), :21
     template <class S> RS_DEV void skip_second(S &s, Tally &t) const {
         if (kind == GK_T) gamma_sample(s, z, ga, t);
         else gamma_sample(s, z, gb, t);
+    }
+    // Attempt-level machine (kinds gamma / beta / f): one Marsaglia-Tsang attempt per call,
+    // its two words drawn at one call site, so the lanes of a warp run the engine and the
+    // common attempt (fast-path normal, t > 0, squeeze / screened acceptance) in step
+    // whatever sample each is in; the sample-level loop ran the normal-word and the
+    // uniform-word engine steps as two divergent sites. Returns true when a sample
+    // completes (value in out); words, tallies and values equal sample()'s.
+    RS_DEV bool am_applies() const { return kind != GK_T; }
+    template <class S> RS_DEV bool am_step(GammaAM &m, S &s, Tally &t, double &out) const {
+        const bool second = m.role != 0;
+        GammaPrm g;
+        g.d = second ? gb.d : ga.d;
+        g.cc = second ? gb.cc : ga.cc;
+        g.td = second ? gb.td : ga.td;
+        g.alpha = second ? gb.alpha : ga.alpha;
+        g.theta = second ? gb.theta : ga.theta;
+        g.boost = second ? gb.boost : ga.boost;
+        const u64 w1 = s.next(), w2 = s.next();
+        const u32 idx = (u32)(w1 & 0xFF);
+        const u64 rabs = (w1 >> 9) & ((1ULL << 52) - 1);
+        const ZigFast f = z.fast[idx];
+        double zn = (double)rabs * f.w;
+        if ((w1 >> 8) & 1) zn = -zn;
+        double tt = 1.0 + g.cc * zn;
+        t.gamma_att++;
+        u64 uw = w2;
+        if (__builtin_expect(rabs < f.k && tt > 0.0, 1)) {
+            t.norm_att++;
+        } else {  // a slow / tail normal token, or t <= 0: the exact normal draw(s) from w1 on
+            PairSrc<S> ps{w1, w2, 0, &s};
+            do {
+                zn = std_norm(ps, z, t);
+                tt = 1.0 + g.cc * zn;
+            } while (!(tt > 0.0));
+            uw = ps.next();
+        }
+        const double v = tt * tt * tt;
+        const double u = u01_of(uw, z.fm);
+        const double zz = zn * zn;
+        double val = g.td * v;
+        if (!(u < 1.0 - 0.0331 * zz * zz || gamma_accept(u, zz, v, g))) return false;
+        if (g.boost) val = g.theta * val * det_exp_dev(det_log_dev(u01_of(s.next(), z.fm)) / g.alpha);
+        if (kind == GK_GAMMA) {
+            out = val;
+            return true;
+        }
+        if (!second) {
+            m.x = val;
+            m.role = 1;
+            return false;
+        }
+        m.role = 0;
+        if (m.lone) {  // the phase-1 parse's lone second sub-sample: a boundary, no sample
+            m.lone = 0;
+            out = 0.0;
+            return true;
+        }
+        out = kind == GK_BETA ? m.x / (m.x + val) : (m.x / nu1) / (val / nu2);
+        return true;
     }
     template <class S> RS_DEV double sample(S &s, Tally &t) const {
         if (kind == GK_T) {

@@ -49,7 +49,8 @@ struct DevCtx {
     size_t cap_T = 0;
     u64 *states = nullptr, *cnt0 = nullptr, *cnt1 = nullptr, *cnt = nullptr, *off = nullptr;
     u32 *ex0 = nullptr, *ex1 = nullptr, *exA = nullptr, *exB = nullptr, *entry = nullptr;
-    u32 *bm = nullptr;  // [2][BM_WORDS][T] boundary bitmaps
+    u32 *bm = nullptr;  // [2][bmw][T] boundary bitmaps
+    size_t bm_bytes = 0;
     void *cub_tmp = nullptr;
     size_t cub_bytes = 0;
     DevResult *res = nullptr;
@@ -113,7 +114,6 @@ rs_status ensure_scratch(DevCtx &c, size_t T) {
     size_t nT = T + T / 4;
     cudaFree(c.states); cudaFree(c.cnt0); cudaFree(c.cnt1); cudaFree(c.cnt); cudaFree(c.off);
     cudaFree(c.ex0); cudaFree(c.ex1); cudaFree(c.exA); cudaFree(c.exB); cudaFree(c.entry); cudaFree(c.cub_tmp);
-    cudaFree(c.bm);
     CK(cudaMalloc(&c.states, nT * 32));
     CK(cudaMalloc(&c.cnt0, nT * 8));
     CK(cudaMalloc(&c.cnt1, nT * 8));
@@ -124,7 +124,6 @@ rs_status ensure_scratch(DevCtx &c, size_t T) {
     CK(cudaMalloc(&c.exA, nT * 4));
     CK(cudaMalloc(&c.exB, nT * 4));
     CK(cudaMalloc(&c.entry, nT * 4));
-    CK(cudaMalloc(&c.bm, nT * 4 * 2 * BM_WORDS));
     c.cub_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, c.cub_bytes, c.cnt, c.off, (int)nT);
     CK(cudaMalloc(&c.cub_tmp, c.cub_bytes));
@@ -750,7 +749,20 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
             p.overrun = c.overrun;
             p.nwords = nw;
         }
-        p.bm = r.family == FAM_GAMMA ? c.bm : nullptr;  // read now: the steps above may grow the scratch
+        p.bm = nullptr;
+        if (r.family == FAM_GAMMA) {
+            // the count pass's boundary bitmaps cover the whole segment (+ the exit overshoot
+            // of 32 units): a fixup then never falls back to re-parsing from the start
+            p.bmw = (u32)((p.L * u + 63) / 32);
+            size_t need = (size_t)p.T * 4 * 2 * p.bmw;
+            if (need > c.bm_bytes) {
+                cudaFree(c.bm);
+                c.bm = nullptr;
+                CK(cudaMalloc(&c.bm, need));
+                c.bm_bytes = need;
+            }
+            p.bm = c.bm;
+        }
         CK(cudaMemsetAsync(c.res, 0, offsetof(DevResult, serial_state), st));
         unsigned g = p.T / BLOCK;
         int round = 0;

@@ -26,11 +26,11 @@ namespace {
 
 constexpr int BLOCK = 256;
 // Gamma-family parses converge only after ~10^2 words, so the count
-// pass records where its parses put sample boundaries in the first BM_WORDS * 32
-// units of the segment; the fixup then re-parses from the true entry alone and looks
-// the meeting point up instead of re-running the speculative parses beside it.
-constexpr u32 BM_WORDS = 32;
-constexpr u64 BM_UNITS = 32 * BM_WORDS;
+// pass records where its parses put sample boundaries, over the whole segment
+// (p.bmw 32-unit words per thread); the fixup then re-parses from the true entry alone
+// and looks the meeting point up instead of re-running the speculative parses beside
+// it. (A 1024-unit window made the rare threads that met later restart both parses
+// from the segment start: gamma 2^26 fixup 1.04 ms.)
 constexpr int MAXLEV = 24;
 constexpr int CAP = RS_BUFFER_CAPACITY;
 
@@ -64,7 +64,8 @@ struct FillPlan {
     const u64 *x256_states;
     const u64 *words;             // materialized engine words (RS_ENG_MEM parse source)
     u64 nwords;
-    u32 *bm;                      // gamma family: count-pass boundary bitmaps (see BM_WORDS)
+    u32 *bm;                      // gamma family: count-pass boundary bitmaps [2][bmw][T]
+    u32 bmw;                      // 32-unit bitmap words per thread and phase
     u32 *overrun;                 // RS_ENG_MEM: set when a parse reads past the materialized words
     const RsZigSlow *zslow;
     const ZigFast *zfast;
@@ -489,27 +490,29 @@ __device__ __forceinline__ void wl_emit(const D &d, SRC &s, u64 kmax, W &wr, Tal
 // ----------------------------------------------------------------------------- two-pass parse
 // boundary bitmap writer: bit q of the segment's map = a sample starts at start + q
 struct BmRec {
-    u32 *bm;  // [BM_WORDS][T]
+    u32 *bm;  // [W][T]
     u32 T, t;
     u64 start;
+    u32 W;
     u32 acc = 0, kw = 0;
     __device__ __forceinline__ void put(u64 pos) {
         u64 q = pos - start;
-        if (!bm || q >= BM_UNITS) return;
+        if (!bm || q >= 32ULL * W) return;
         u32 k = (u32)(q >> 5);
         while (kw < k) { bm[(size_t)kw * T + t] = acc; acc = 0; kw++; }
         acc |= 1u << (q & 31);
     }
     __device__ __forceinline__ void close() {
         if (!bm) return;
-        while (kw < BM_WORDS) { bm[(size_t)kw * T + t] = acc; acc = 0; kw++; }
+        while (kw < W) { bm[(size_t)kw * T + t] = acc; acc = 0; kw++; }
     }
 };
-// samples of a recorded parse that start before unit q (q < BM_UNITS)
+// samples of a recorded parse that start before unit q (q < 32 * bmw)
 __device__ __forceinline__ u64 bm_rank(const u32 *bm, u32 T, u32 t, u64 q) {
     u32 k = (u32)(q >> 5);
     u64 r = 0;
-    for (u32 j = 0; j < k; j++) r += __popc(bm[(size_t)j * T + t]);
+#pragma unroll 8
+    for (u32 j = 0; j < k; j++) r += __popc(__ldg(&bm[(size_t)j * T + t]));
     return r + __popc(bm[(size_t)k * T + t] & ((1u << (q & 31)) - 1u));
 }
 // count: samples that START inside [seg_start, seg_end) and the exit (first sample
@@ -550,12 +553,24 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_count(const __grid_consta
         }
         if (!done) {
             if constexpr (D == FAM_GAMMA) {
-                BmRec r{p.bm, p.T, t, seg_start(p, t)};
+                BmRec r{p.bm, p.T, t, seg_start(p, t), p.bmw};
                 r.put(r.start);  // phase 0 starts a sample at the segment start
-                while (s.pos < end) {
-                    d.sample(s, tl);
-                    c++;
-                    r.put(s.pos);
+                if (d.am_applies()) {  // attempt-level machine (same samples and positions)
+                    GammaAM m{0, 0, 0.0};
+                    while (true) {
+                        double v;
+                        if (d.am_step(m, s, tl, v)) {
+                            c++;
+                            r.put(s.pos);
+                            if (s.pos >= end) break;
+                        }
+                    }
+                } else {
+                    while (s.pos < end) {
+                        d.sample(s, tl);
+                        c++;
+                        r.put(s.pos);
+                    }
                 }
                 r.close();
             } else {
@@ -568,14 +583,30 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_count(const __grid_consta
         if (d.paired()) {
             typename SrcOf<E, D>::type s1;
             make_src<E>(p, t, seg_start(p, t), s1);
-            d.skip_second(s1, tl);
             u64 c1 = 0;
-            BmRec r{p.bm ? p.bm + (size_t)BM_WORDS * p.T : nullptr, p.T, t, seg_start(p, t)};
-            r.put(s1.pos);  // phase 1's first full sample starts after the lone second
-            while (s1.pos < end) {
-                d.sample(s1, tl);
-                c1++;
-                r.put(s1.pos);
+            BmRec r{p.bm ? p.bm + (size_t)p.bmw * p.T : nullptr, p.T, t, seg_start(p, t), p.bmw};
+            bool am = false;
+            if constexpr (D == FAM_GAMMA) am = d.am_applies();
+            if (am) {
+                if constexpr (D == FAM_GAMMA) {
+                    GammaAM m{1, 1, 0.0};  // a lone second sub-sample first
+                    double v;
+                    while (!d.am_step(m, s1, tl, v)) {}
+                    r.put(s1.pos);  // phase 1's first full sample starts after the lone second
+                    while (s1.pos < end) {
+                        while (!d.am_step(m, s1, tl, v)) {}
+                        c1++;
+                        r.put(s1.pos);
+                    }
+                }
+            } else {
+                d.skip_second(s1, tl);
+                r.put(s1.pos);  // phase 1's first full sample starts after the lone second
+                while (s1.pos < end) {
+                    d.sample(s1, tl);
+                    c1++;
+                    r.put(s1.pos);
+                }
             }
             r.close();
             cnt1[t] = c1;
@@ -602,7 +633,7 @@ __device__ void resolve_entry(const FillPlan &p, const ZigFast *sm, u32 t, u32 e
             make_dist<D>(p, sm, d);
             Tally tl;
             const bool two = d.paired();
-            const u32 *bm0 = p.bm, *bm1 = p.bm + (size_t)BM_WORDS * p.T;
+            const u32 *bm0 = p.bm, *bm1 = p.bm + (size_t)p.bmw * p.T;
             u64 nb = 0;
             u32 kw = ~0u, wa = 0, wc = 0;
             while (true) {
@@ -612,7 +643,7 @@ __device__ void resolve_entry(const FillPlan &p, const ZigFast *sm, u32 t, u32 e
                     return;
                 }
                 u64 q = sb.pos - start;
-                if (q >= BM_UNITS) break;
+                if (q >= 32ULL * p.bmw) break;
                 u32 k = (u32)(q >> 5), bit = 1u << (q & 31);
                 if (k != kw) {
                     kw = k;
@@ -750,6 +781,21 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constan
                         BatchRing<T, BLOCK> wr;
                         wr.init((T *)p.out, p.out0 + o, ring);
                         wl_emit(d, s, kmax, wr, tl);
+                        wr.finish();
+                        done = true;
+                    }
+                }
+                if constexpr (D == FAM_GAMMA) {
+                    if (d.am_applies()) {  // one attempt per step, <= 1 sample
+                        BatchRing<T, BLOCK> wr;
+                        wr.init((T *)p.out, p.out0 + o, ring);
+                        GammaAM m{0, 0, 0.0};
+                        u32 it = 0;
+                        for (u64 k = 0; k < kmax;) {
+                            double v;
+                            if (d.am_step(m, s, tl, v)) { wr.put(v); k++; }
+                            if ((++it & (BatchRing<T, BLOCK>::G - 1)) == 0) wr.tick();
+                        }
                         wr.finish();
                         done = true;
                     }
