@@ -515,6 +515,14 @@ __device__ __forceinline__ u64 bm_rank(const u32 *bm, u32 T, u32 t, u64 q) {
     for (u32 j = 0; j < k; j++) r += __popc(__ldg(&bm[(size_t)j * T + t]));
     return r + __popc(bm[(size_t)k * T + t] & ((1u << (q & 31)) - 1u));
 }
+// bm_rank over bitmaps the calling thread wrote itself in this kernel (no __ldg)
+__device__ __forceinline__ u64 bm_rank_own(const u32 *bm, u32 T, u32 t, u64 q) {
+    u32 k = (u32)(q >> 5);
+    u64 r = 0;
+#pragma unroll 8
+    for (u32 j = 0; j < k; j++) r += __popc(bm[(size_t)j * T + t]);
+    return r + __popc(bm[(size_t)k * T + t] & ((1u << (q & 31)) - 1u));
+}
 // count: samples that START inside [seg_start, seg_end) and the exit (first sample
 // boundary at or beyond seg_end), parsing from seg_start as if it were a boundary.
 // For paired samplers (beta, f, t, skew_normal: two sub-samples per sample) a parse
@@ -587,13 +595,27 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_count(const __grid_consta
             BmRec r{p.bm ? p.bm + (size_t)p.bmw * p.T : nullptr, p.T, t, seg_start(p, t), p.bmw};
             bool am = false;
             if constexpr (D == FAM_GAMMA) am = d.am_applies();
+            bool merged = false;
             if (am) {
                 if constexpr (D == FAM_GAMMA) {
                     GammaAM m{1, 1, 0.0};  // a lone second sub-sample first
                     double v;
                     while (!d.am_step(m, s1, tl, v)) {}
                     r.put(s1.pos);  // phase 1's first full sample starts after the lone second
+                    // Once phase 1 starts a sample where phase 0 did, the two parses coincide
+                    // to the segment end: the rest of phase 1's count is phase 0's, read off
+                    // the phase-0 bitmap this thread just wrote (plain loads: own stores).
+                    const u32 *b0 = p.bm;
+                    const u64 st0 = seg_start(p, t);
                     while (s1.pos < end) {
+                        if (b0) {
+                            const u64 q = s1.pos - st0;
+                            if ((b0[(size_t)(q >> 5) * p.T + t] >> (q & 31)) & 1) {
+                                c1 += c - bm_rank_own(b0, p.T, t, q);
+                                merged = true;
+                                break;
+                            }
+                        }
                         while (!d.am_step(m, s1, tl, v)) {}
                         c1++;
                         r.put(s1.pos);
@@ -610,7 +632,7 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_count(const __grid_consta
             }
             r.close();
             cnt1[t] = c1;
-            ex1[t] = (u32)(s1.pos - end);
+            ex1[t] = merged ? (u32)(s.pos - end) : (u32)(s1.pos - end);
         }
     }
     cnt0[t] = c;
