@@ -682,7 +682,13 @@ __device__ void resolve_entry(const FillPlan &p, const ZigFast *sm, u32 t, u32 e
                     ex = x1;
                     return;
                 }
-                d.sample(sb, tl);
+                if (d.am_applies()) {  // one sample through the attempt-level machine
+                    GammaAM m{0, 0, 0.0};
+                    double v;
+                    while (!d.am_step(m, sb, tl, v)) {}
+                } else {
+                    d.sample(sb, tl);
+                }
                 nb++;
             }
         }  // no meeting in the recorded window: the lockstep parse below
