@@ -446,6 +446,8 @@ RS_DEV void rlx_mulmod_dev(const u64 *x, const u64 *y, u64 *out) {
     for (int i = 0; i < 9; i++) out[i] = q[i];
 }
 
+#include "rs_ranlux_mul.cuh"  // rlx_mul_A: the engine step with the fixed multiplier
+
 struct EngRanlux {  // words of a chunk: the 9 limbs of the new residue, low first
     u64 x[9];
     u64 o[9];
@@ -453,10 +455,7 @@ struct EngRanlux {  // words of a chunk: the 9 limbs of the new residue, low fir
     const u64 *A;  // multiplier limbs (global)
     RS_DEV u64 next() {
         if (left == 0) {
-            u64 a[9];
-#pragma unroll
-            for (int i = 0; i < 9; i++) a[i] = __ldg(A + i);
-            rlx_mulmod_dev(x, a, x);
+            rlx_mul_A(x, x);
 #pragma unroll
             for (int i = 0; i < 9; i++) o[i] = x[i];
             left = 9;
