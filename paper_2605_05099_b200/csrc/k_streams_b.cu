@@ -11,6 +11,7 @@ const void *streams_e(int fam) {
     case FAM_F32: return (const void *)k_streams<E, FAM_F32>;
     case FAM_U32: return (const void *)k_streams<E, FAM_U32>;
     case FAM_FIXED: return (const void *)k_streams<E, FAM_FIXED>;
+    case FAM_LEMIRE_RING: return (const void *)k_streams<E, FAM_LEMIRE_RING>;
     default: return (const void *)k_streams<E, FAM_LEMIRE>;
     }
 }

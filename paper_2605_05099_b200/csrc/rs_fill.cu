@@ -1023,10 +1023,15 @@ rs_status rs_fill_streams(int32_t engine, const uint64_t *seed, int32_t n_seed, 
         a.fmode = r.fixed_mode;
         memcpy(a.ip, r.ip, sizeof a.ip);
     }
+    // Lemire with a rejection zone above 1/16 of the words (b close above a power of two,
+    // e.g. 2^63+1): the word-level chunk ring; otherwise the unrolled 32-sample chunks, whose
+    // smaller tile keeps 2^16 streams in one wave
+    if (d == FAM_LEMIRE && a.ip[1] > (1ULL << 60)) d = FAM_LEMIRE_RING;
     const void *fn = rsk::streams_kernel(engine, d);
     void *args[] = {&a};
     unsigned g2 = (unsigned)((n_streams + STR_BLOCK - 1) / STR_BLOCK);
-    if ((rc = launch(fn, dim3(g2), dim3(STR_BLOCK), args, st, ST_SMEM))) return rc;
+    if ((rc = launch(fn, dim3(g2), dim3(STR_BLOCK), args, st, d == FAM_LEMIRE_RING ? ST_SMEM_RING : ST_SMEM)))
+        return rc;
     if (sg.host) {
         CK(cudaMemcpyAsync(out, sg.dptr, bytes, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));

@@ -280,7 +280,8 @@ __device__ __forceinline__ void make_src(const FillPlan &p, u32 t, u64 hpos, HSr
 
 // ---- sampler families (template key) and their construction from the plan
 enum { FAM_LEMIRE = RS_DIST_UINT64, FAM_NORM = RS_DIST_NORM, FAM_EXP = RS_DIST_EXP, FAM_GAMMA = RS_DIST_GAMMA,
-       FAM_F32 = 11, FAM_U32 = 22, FAM_FIXED = 40 /* per-stream mode: a fixed map of each word */ };
+       FAM_F32 = 11, FAM_U32 = 22, FAM_FIXED = 40 /* per-stream mode: a fixed map of each word */,
+       FAM_LEMIRE_RING = 41 /* per-stream mode: Lemire rows through the word-level chunk ring */ };
 template <int D> struct DistOf;
 template <> struct DistOf<FAM_NORM> { typedef DistNorm type; };
 template <> struct DistOf<FAM_EXP> { typedef DistExp type; };
@@ -897,6 +898,7 @@ __device__ __forceinline__ u64 fx_map(const PL &p, u64 w) {
 // 4.6 TB/s with 128-byte ones (exp/wpeak2.cu). The ragged head (up to line
 // alignment, and the buffered prefix) and tail are scalar.
 constexpr int FX_CH = 32;
+constexpr int LR_ROW = 65;  // per-stream Lemire rows: a 64-sample ring per lane (two chunks), padded
 // Row stride 33 words: the lanes' row-wise STS.64 are conflict-free and the store
 // phase's LDS.64 pairs 2-way conflicted. An XOR-swizzled unpadded layout (conflict-free
 // LDS.128) measured slower -- 1.80 vs 1.51 ms for x256** 2^30 -- because its per-word
@@ -1318,10 +1320,59 @@ __device__ __forceinline__ void stream_rows8(u64 *out, u64 j, u64 nper, bool val
         for (u64 i = nch * FX_CH; i < nper; i++) out[j * nper + i] = produce();
 }
 
+// Per-stream Lemire rows (rejections: a lane needs a variable number of words per
+// sample): every lane consumes one word per step and appends accepted samples to a
+// 64-slot ring (its tile row); every 32 steps the warp stores the rows that hold a full
+// 32-sample chunk, two lanes' 256-byte chunks per STG.128 instruction (rows without one
+// sit the store out). A lane adds <= 32 samples between stores, so the ring never holds
+// more than 63. The per-sample redraw loop instead kept every lane waiting for the
+// warp's slowest sample (m = 2^63 + 1 rejects half of the words).
+template <class D, class EN>
+__device__ __forceinline__ void stream_rows_lemire(u64 *out, u64 j, u64 nper, bool valid, u64 *tile, const D &d,
+                                                   EN &e) {
+    const u32 lane = threadIdx.x & 31;
+    u64 *ring = tile + lane * LR_ROW;
+    u64 k = 0, stored = 0;  // samples produced / stored (stored: whole chunks)
+    const u64 nch = nper / FX_CH;
+    const u64 row = (u64)(uintptr_t)(out + j * nper);
+    for (u32 it = 1;; it++) {
+        if (valid && k < nper) {
+            u64 o;
+            if (d.accept(e.next(), o)) {
+                ring[k & 63] = o;
+                k++;
+            }
+        }
+        if ((it & 31) == 0) {
+            const bool ready = valid && k - stored >= FX_CH && stored < nch * FX_CH;
+            const u64 dst = ready ? row + stored * 8 : 0;
+            const u32 base = (u32)(stored & 63);
+            __syncwarp();
+#pragma unroll
+            for (int g = 0; g < 16; g++) {
+                u32 r = 2 * g + (lane >> 4), c = lane & 15;
+                u64 dd = __shfl_sync(0xFFFFFFFFu, dst, r);
+                u32 bb = __shfl_sync(0xFFFFFFFFu, base, r);
+                if (dd) {
+                    u64 x = tile[r * LR_ROW + bb + 2 * c], y = tile[r * LR_ROW + bb + 2 * c + 1];
+                    asm volatile("st.global.v2.b64 [%0], {%1, %2};" ::"l"(dd + 16 * c), "l"(x), "l"(y) : "memory");
+                }
+            }
+            __syncwarp();
+            if (ready) stored += FX_CH;
+            const bool more = valid && (k < nper || stored < nch * FX_CH);
+            if (!__any_sync(0xFFFFFFFFu, more)) break;
+        }
+    }
+    if (valid)
+        for (u64 i = stored; i < nper; i++) out[j * nper + i] = ring[i & 63];  // the tail (< 32)
+}
+
 // 64-thread blocks: one thread per stream cannot be split (sfc64 has no skip-ahead), so
 // small blocks spread the few warps evenly over the SMs (2^16 streams: 13.8 warps/SM)
 constexpr int STR_BLOCK = 64;
-constexpr size_t ST_SMEM = (size_t)(STR_BLOCK / 32) * 32 * FX_ROW * 8;  // dynamic shared memory of k_streams
+constexpr size_t ST_SMEM = (size_t)(STR_BLOCK / 32) * 32 * FX_ROW * 8;   // dynamic shared memory of k_streams
+constexpr size_t ST_SMEM_RING = (size_t)(STR_BLOCK / 32) * 32 * LR_ROW * 8;  // ... with a.ring
 template <int E, int D>
 __global__ void __launch_bounds__(STR_BLOCK) k_streams(const __grid_constant__ StreamArgs a) {
     __shared__ ZigFast sm[256];
@@ -1335,12 +1386,12 @@ __global__ void __launch_bounds__(STR_BLOCK) k_streams(const __grid_constant__ S
     // 8-byte rows through the warp tile (whole warps: no early exit) when every row
     // start is 16-byte aligned; otherwise the per-thread writers below
     extern __shared__ __align__(16) u64 st_dyn[];  // ST_SMEM
-    constexpr bool W8 = sizeof(typename DistOf<D == FAM_FIXED ? FAM_LEMIRE : D>::type::out_t) == 8;
+    constexpr bool W8 = sizeof(typename DistOf<(D == FAM_FIXED || D == FAM_LEMIRE_RING) ? FAM_LEMIRE : D>::type::out_t) == 8;
     const bool tiled = W8 && !(D == FAM_FIXED && is_half(a.fmode)) && a.nper % 2 == 0 &&
                        (((uintptr_t)a.out) & 15) == 0;
     if (!tiled && j >= a.nstreams) return;
     const bool valid = j < a.nstreams;
-    u64 *tile = st_dyn + (threadIdx.x >> 5) * 32 * FX_ROW;
+    u64 *tile = st_dyn + (threadIdx.x >> 5) * 32 * (D == FAM_LEMIRE_RING ? LR_ROW : FX_ROW);
     u64 w[9];
     typename EngOf<E>::type e;
     if (valid) {
@@ -1407,15 +1458,17 @@ __global__ void __launch_bounds__(STR_BLOCK) k_streams(const __grid_constant__ S
         }
         return;
     }
-    typedef typename DistOf<D == FAM_FIXED ? FAM_LEMIRE : D>::type DT;
+    typedef typename DistOf<(D == FAM_FIXED || D == FAM_LEMIRE_RING) ? FAM_LEMIRE : D>::type DT;
     DT d;
     DistArgs da{a.fp, a.ip, &a.ga, &a.gb, a.kind, a.fm, a.zslow, a.zslowf};
-    make_dist_a<D == FAM_FIXED ? FAM_LEMIRE : D>(da, sm, d);
+    make_dist_a<(D == FAM_FIXED || D == FAM_LEMIRE_RING) ? FAM_LEMIRE : D>(da, sm, d);
     typedef typename DT::out_t T;
     Tally tl;
     if constexpr (sizeof(T) == 8) {
         if (tiled) {
-            if constexpr (D == FAM_LEMIRE) {
+            if constexpr (D == FAM_LEMIRE_RING) {
+                stream_rows_lemire((u64 *)a.out, j, a.nper, valid, tile, d, e);
+            } else if constexpr (D == FAM_LEMIRE) {  // (almost) no rejections: unrolled 32-sample chunks
                 stream_rows8((u64 *)a.out, j, a.nper, valid, tile, [&]() {
                     u64 o;
                     while (!d.accept(e.next(), o)) {}

@@ -250,7 +250,7 @@ def test_streams_tiled_rows(engine):
     """8-byte rows through the warp tile (even row length): partial warps (45 streams),
     rows that are not whole 32-sample chunks, and the caller's out= tensor."""
     for dist, params, n in (("uint64", {}, 1002), ("u01", {}, 64), ("norm", {}, 994), ("uint64", {"b": 10}, 130),
-                            ("exp", {}, 2)):
+                            ("exp", {}, 2), ("uint64", {"b": (1 << 63) + 1}, 1002), ("uint64", {"b": (1 << 63) + 5}, 64)):
         out = fill_streams(engine, [11], [], 2, 45, dist, params, n)
         again = torch.empty_like(out)
         assert fill_streams(engine, [11], [], 2, 45, dist, params, n, out=again) is again
