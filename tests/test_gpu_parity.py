@@ -294,6 +294,22 @@ def test_mvn(golden_arrays, d, n, layout):
         assert np.max(np.abs(X0 - ref0)) <= 1e-12 * np.max(np.abs(ref0))
 
 
+def test_mvn_zero_mean_triangular():
+    """n_d with a Cholesky factor at d >= 192 takes the TRMM, and a zero mean skips the add."""
+    d, n = 256, 512
+    r = state_io.create("philox", seed=[4])
+    o = O.OracleRng("philox", seed=[4])
+    B = np.random.default_rng(9).standard_normal((d, d))
+    S = B @ B.T / d + np.eye(d)
+    X = _np(r.mvn(np.zeros(d), S, n=n))
+    L = np.linalg.cholesky(S)
+    z = o.fill("stdnorm", {}, n * d).reshape(n, d)
+    ref = np.zeros(d) + z @ L.T
+    scale = np.abs(z) @ np.abs(L).T
+    assert np.max(np.abs(X - ref) / scale) <= 1e-12
+    _assert_same_position(r, o)
+
+
 @pytest.mark.parametrize("layout", ["n_d", "d_n"])
 def test_mvn_semidefinite(layout):
     """rank-deficient covariance: the pivoted (non-triangular) factor of continuous.py:293-309
