@@ -162,6 +162,49 @@ rs_status rs_fill_streams(int32_t engine, const uint64_t *seed, int32_t n_seed,
 rs_status rs_mvn(rs_stream *stream, const double *L, const double *mean, int64_t d, uint64_t n,
                  int32_t layout, double *out, rs_fill_result *result, void *cuda_stream);
 
+/* ---- multi-GPU sharding of variable-consumption fills ----
+ * Replaces nothing one-for-one in the reference: it is the rank-local half of
+ * `Rng.fill(dist, params, n)` (rng.py:223-241) when one logical stream is split
+ * into contiguous word slices, one per GPU (paper_2605_05099_b200/shard.py runs
+ * the protocol: warm-up entry guess, count, exchange of (entry, exit, count),
+ * re-count on a mismatch, prefix offsets, emit). A slice is seg_len * n_seg
+ * engine words of a stream positioned at its start (fresh: no buffered words,
+ * no pending half); its samples are those that START at a unit position in
+ * [entry, units(slice)), units = words, or 32-bit halves for the f32 laws. */
+#define RS_RANGE_ALIGN 72 /* seg_len multiple: Philox blocks (4), ranlux chunks (9), 8-lane interleave */
+
+typedef struct rs_dist_info_t {
+    int32_t unit;              /* 1: 64-bit words, 2: 32-bit halves */
+    int32_t variable;          /* 1: variable consumption (rejection samplers), 0: one unit per sample */
+    double words_per_sample;   /* provisioning estimate (64-bit words per sample) */
+    uint64_t min_seg_len;      /* shortest segment a range plan uses (multiple of RS_RANGE_ALIGN) */
+    int32_t tally_seen[3];     /* which of the norm/exp/gamma tallies the law touches */
+    int32_t pad;
+} rs_dist_info_t;
+
+typedef struct rs_range_info {
+    uint64_t count;            /* samples starting in [entry, units(slice)) */
+    uint64_t exit;             /* first sample boundary at or past the slice end, in units past it */
+    uint64_t end_pos;          /* after rs_range_emit(keep > 0): unit position (from the slice start)
+                                  right after sample keep-1; else entry */
+    uint64_t tally[6];         /* emitted samples' tallies (rs_fill_result layout) */
+    int32_t unit;
+    int32_t resync_rounds;
+} rs_range_info;
+
+/* validated law description (host only, no device needed) */
+rs_status rs_dist_info(int32_t dist, const double *fparams, const uint64_t *iparams, rs_dist_info_t *info);
+/* slice shape for >= `words` engine words on the current device: one wave of segments */
+rs_status rs_range_geometry(int32_t engine, int32_t dist, const double *fparams, const uint64_t *iparams,
+                            uint64_t words, uint64_t *seg_len, uint32_t *n_seg);
+/* count + exit of one slice (synchronous); keeps the plan for rs_range_emit on this device */
+rs_status rs_range_count(const rs_stream *stream, int32_t dist, const double *fparams,
+                         const uint64_t *iparams, uint64_t entry, uint64_t seg_len, uint32_t n_seg,
+                         rs_range_info *info, void *cuda_stream);
+/* write the first `keep` samples of the counted slice into device memory (synchronous).
+ * Any other fill on the device between count and emit invalidates the slice (RS_ERR_VALUE). */
+rs_status rs_range_emit(uint64_t keep, void *out_device, rs_range_info *info, void *cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -49,6 +49,31 @@ class RsFillResult(ctypes.Structure):
     ]
 
 
+class RsDistInfo(ctypes.Structure):
+    _fields_ = [
+        ("unit", ctypes.c_int32),
+        ("variable", ctypes.c_int32),
+        ("words_per_sample", ctypes.c_double),
+        ("min_seg_len", ctypes.c_uint64),
+        ("tally_seen", ctypes.c_int32 * 3),
+        ("pad", ctypes.c_int32),
+    ]
+
+
+class RsRangeInfo(ctypes.Structure):
+    _fields_ = [
+        ("count", ctypes.c_uint64),
+        ("exit", ctypes.c_uint64),
+        ("end_pos", ctypes.c_uint64),
+        ("tally", ctypes.c_uint64 * 6),
+        ("unit", ctypes.c_int32),
+        ("resync_rounds", ctypes.c_int32),
+    ]
+
+
+RANGE_ALIGN = 72  # RS_RANGE_ALIGN
+
+
 class LibraryError(RuntimeError):
     pass
 
@@ -83,6 +108,14 @@ def _load():
                                   ctypes.c_void_p]
     L.rs_mvn.argtypes = [ctypes.POINTER(RsStream), ctypes.c_void_p, DBLP, ctypes.c_int64, ctypes.c_uint64,
                          ctypes.c_int32, ctypes.c_void_p, ctypes.POINTER(RsFillResult), ctypes.c_void_p]
+    L.rs_dist_info.argtypes = [ctypes.c_int32, DBLP, U64P, ctypes.POINTER(RsDistInfo)]
+    L.rs_range_geometry.argtypes = [ctypes.c_int32, ctypes.c_int32, DBLP, U64P, ctypes.c_uint64, U64P,
+                                    ctypes.POINTER(ctypes.c_uint32)]
+    L.rs_range_count.argtypes = [ctypes.POINTER(RsStream), ctypes.c_int32, DBLP, U64P, ctypes.c_uint64,
+                                 ctypes.c_uint64, ctypes.c_uint32, ctypes.POINTER(RsRangeInfo), ctypes.c_void_p]
+    L.rs_range_emit.argtypes = [ctypes.c_uint64, ctypes.c_void_p, ctypes.POINTER(RsRangeInfo), ctypes.c_void_p]
+    for name in ("rs_dist_info", "rs_range_geometry", "rs_range_count", "rs_range_emit"):
+        getattr(L, name).restype = ctypes.c_int
     for name in ("rs_init_device", "rs_seed_words", "rs_engine_seed", "rs_engine_seed_from", "rs_engine_check_state",
                  "rs_engine_generate", "rs_engine_jump", "rs_engine_advance_words", "rs_pcg_advance", "rs_fill",
                  "rs_fill_async", "rs_fill_streams", "rs_mvn"):
@@ -99,6 +132,7 @@ EXPORTED = (
     "rs_engine_seed_words", "rs_engine_chunk", "rs_seed_words", "rs_engine_seed", "rs_engine_seed_from",
     "rs_engine_check_state", "rs_engine_generate", "rs_engine_jump", "rs_engine_advance_words", "rs_pcg_advance",
     "rs_fill", "rs_fill_async", "rs_fill_streams", "rs_mvn",
+    "rs_dist_info", "rs_range_geometry", "rs_range_count", "rs_range_emit",
 )
 
 

@@ -64,6 +64,17 @@ struct DevCtx {
     u64 *words = nullptr;  // materialized engine words for parse-from-memory
     size_t words_bytes = 0;
     u32 *overrun = nullptr;  // device flag: a parse read past the materialized words
+    // the counted slice of rs_range_count, waiting for rs_range_emit (its plan refers to
+    // the scratch above, so any other fill on this device invalidates it)
+    struct Range {
+        bool valid = false;
+        FillPlan p;
+        rsk::VarKernels K;
+        u32 *ex = nullptr;
+        u64 count = 0;
+        int unit = 1;
+        bool mem = false;
+    } range;
 };
 
 std::mutex g_mu;
@@ -441,18 +452,24 @@ void fill_plan_common(FillPlan &p, DevCtx &c, const Resolved &r, int engine, int
 
 // Segment geometry + per-engine jump tables for stride L (engine origin = p.base)
 rs_status plan_segments(DevCtx &c, FillPlan &p, u64 words, u64 Lmin, int occ, cudaStream_t st, bool tables = true,
-                        u64 align = 36) {
-    // exactly one wave of resident threads: equal segments finish together
-    u64 Tfull = (u64)c.sms * (u64)occ * BLOCK;
-    u64 L = (words + Tfull - 1) / Tfull;
-    if (L < Lmin) L = Lmin;
-    // a whole number of philox blocks (4) and ranlux chunks (9); fixed fills pass
-    // align = 144 (also 16-word lines): every thread then has the same alignment
-    // prologue, so the lanes stay in phase (ranlux mulmods convergent)
-    L = (L + align - 1) / align * align;
-    u64 T = (words + L - 1) / L;
-    if (T < 1) T = 1;
-    T = (T + BLOCK - 1) / BLOCK * BLOCK;
+                        u64 align = 36, u64 force_L = 0, u64 force_T = 0) {
+    u64 L, T;
+    if (force_L) {  // explicit geometry (rs_range_count: every rank's slice has the same shape)
+        L = force_L;
+        T = force_T;
+    } else {
+        // exactly one wave of resident threads: equal segments finish together
+        u64 Tfull = (u64)c.sms * (u64)occ * BLOCK;
+        L = (words + Tfull - 1) / Tfull;
+        if (L < Lmin) L = Lmin;
+        // a whole number of philox blocks (4) and ranlux chunks (9); fixed fills pass
+        // align = 144 (also 16-word lines): every thread then has the same alignment
+        // prologue, so the lanes stay in phase (ranlux mulmods convergent)
+        L = (L + align - 1) / align * align;
+        T = (words + L - 1) / L;
+        if (T < 1) T = 1;
+        T = (T + BLOCK - 1) / BLOCK * BLOCK;
+    }
     p.L = L;
     p.T = (u32)T;
     int levels = 1;
@@ -603,6 +620,56 @@ rs_status launch_raw_words(DevCtx &c, FillPlan &m, cudaStream_t st) {
     return launch(fn, dim3(m.T / BLOCK), dim3(BLOCK), args, st, FX_SMEM);
 }
 
+// shortest segment of a variable-consumption plan (gamma-family resync distances)
+u64 var_lmin(const Resolved &r) { return r.family == FAM_GAMMA ? (r.kind == GK_GAMMA ? 1024 : 2048) : 128; }
+
+// Per-chunk device inputs of the parse passes: the materialized engine words
+// (parse-from-memory engines) and the gamma family's boundary bitmaps.
+rs_status prep_chunk(DevCtx &c, FillPlan &p, const Resolved &r, bool mem, cudaStream_t st) {
+    rs_status rc;
+    if (mem) {
+        // materialize the chunk's engine words (+ slack for the parses that run past the
+        // last segment end) with the coalesced fixed-fill kernel
+        u64 nw = (u64)p.T * p.L + std::max<u64>(1ULL << 16, (u64)p.T * p.L / 64);
+        nw = (nw + 143) / 144 * 144;
+        if (nw * 8 > c.words_bytes) {
+            cudaFree(c.words);
+            c.words = nullptr;
+            CK(cudaMalloc(&c.words, nw * 8));
+            c.words_bytes = nw * 8;
+        }
+        FillPlan m = p;
+        m.P = 0;
+        m.lp0 = 0;
+        m.n = nw;
+        m.weng = nw;
+        m.out = c.words;
+        m.out0 = 0;
+        m.pending_used = 0;
+        m.unit = 1;
+        m.fmode = FX_RAW;
+        if ((rc = launch_raw_words(c, m, st))) return rc;
+        p.words = c.words;
+        p.overrun = c.overrun;
+        p.nwords = nw;
+    }
+    p.bm = nullptr;
+    if (r.family == FAM_GAMMA) {
+        // the count pass's boundary bitmaps cover the whole segment (+ the exit overshoot
+        // of 32 units): a fixup then never falls back to re-parsing from the start
+        p.bmw = (u32)((p.L * (u64)r.unit + 63) / 32);
+        size_t need = (size_t)p.T * 4 * 2 * p.bmw;
+        if (need > c.bm_bytes) {
+            cudaFree(c.bm);
+            c.bm = nullptr;
+            CK(cudaMalloc(&c.bm, need));
+            c.bm_bytes = need;
+        }
+        p.bm = c.bm;
+    }
+    return RS_OK;
+}
+
 // The device part of one fill. On return (sync=true) `E` holds the stream units
 // consumed (64-bit words, or 32-bit halves incl. a used pending half when r.unit == 2)
 // and `tal` the tallies.
@@ -611,6 +678,7 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
     E = 0;
     rounds = 0;
     chunks = 0;
+    c.range.valid = false;
     for (int i = 0; i < 6; i++) tal[i] = 0;
     if (n == 0) return RS_OK;
     FillPlan p;
@@ -698,7 +766,7 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
     u64 done = 0;    // samples produced so far
     u64 origin = 0;  // engine words from s->state to this chunk's origin (multiple of 36)
     u64 lp0 = 0;
-    u64 Lmin = r.family == FAM_GAMMA ? (r.kind == GK_GAMMA ? 1024 : 2048) : 128;
+    u64 Lmin = var_lmin(r);
     bool first = true;
     while (done < n) {
         u64 need = n - done;
@@ -723,46 +791,7 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
         const bool mem = parse_from_memory(s->engine);
         rc = plan_segments(c, p, words + (lp0 + u - 1) / u, Lmin, occ, st, !mem);
         if (rc) return rc;
-        if (mem) {
-            // materialize the chunk's engine words (+ slack for the parses that run past the
-            // last segment end) with the coalesced fixed-fill kernel
-            u64 nw = (u64)p.T * p.L + std::max<u64>(1ULL << 16, (u64)p.T * p.L / 64);
-            nw = (nw + 143) / 144 * 144;
-            if (nw * 8 > c.words_bytes) {
-                cudaFree(c.words);
-                c.words = nullptr;
-                CK(cudaMalloc(&c.words, nw * 8));
-                c.words_bytes = nw * 8;
-            }
-            FillPlan m = p;
-            m.P = 0;
-            m.lp0 = 0;
-            m.n = nw;
-            m.weng = nw;
-            m.out = c.words;
-            m.out0 = 0;
-            m.pending_used = 0;
-            m.unit = 1;
-            m.fmode = FX_RAW;
-            if ((rc = launch_raw_words(c, m, st))) return rc;
-            p.words = c.words;
-            p.overrun = c.overrun;
-            p.nwords = nw;
-        }
-        p.bm = nullptr;
-        if (r.family == FAM_GAMMA) {
-            // the count pass's boundary bitmaps cover the whole segment (+ the exit overshoot
-            // of 32 units): a fixup then never falls back to re-parsing from the start
-            p.bmw = (u32)((p.L * u + 63) / 32);
-            size_t need = (size_t)p.T * 4 * 2 * p.bmw;
-            if (need > c.bm_bytes) {
-                cudaFree(c.bm);
-                c.bm = nullptr;
-                CK(cudaMalloc(&c.bm, need));
-                c.bm_bytes = need;
-            }
-            p.bm = c.bm;
-        }
+        if ((rc = prep_chunk(c, p, r, mem, st))) return rc;
         CK(cudaMemsetAsync(c.res, 0, offsetof(DevResult, serial_state), st));
         unsigned g = p.T / BLOCK;
         int round = 0;
@@ -979,6 +1008,7 @@ rs_status rs_fill_streams(int32_t engine, const uint64_t *seed, int32_t n_seed, 
     }
     DevCtx *c;
     if ((rc = init_dev(dev, &c))) return rc;
+    c->range.valid = false;
     cudaStream_t st = (cudaStream_t)cuda_stream;
     size_t bytes = (size_t)n_streams * n_per_stream * elem_size(dist);
     Staging sg;
@@ -1166,6 +1196,198 @@ rs_status rs_mvn(rs_stream *s, const double *L, const double *mean, int64_t d, u
     if (host_out) CK(cudaMemcpyAsync(out, X, nz * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (result) *result = fr;
+    rs::clear_error();
+    return RS_OK;
+}
+
+// ----------------------------------------------------------------------------- sharded fills
+// One rank's slice of a variable-consumption fill. The stream is at the
+// slice start (fresh: no buffered words, no pending half); the slice is seg_len * n_seg
+// engine words, parsed as n_seg segments; its samples are those that START in
+// [entry, units(slice)). rs_range_count runs count + fixup (+ resolution rounds) + scan
+// and reports the count and the exit; rs_range_emit writes the first `keep` samples.
+
+rs_status rs_dist_info(int32_t dist, const double *fparams, const uint64_t *iparams, rs_dist_info_t *info) {
+    double fz[4] = {0, 0, 0, 0};
+    u64 iz[4] = {0, 0, 0, 0};
+    Resolved r;
+    rs_status rc = resolve(dist, fparams ? fparams : fz, iparams ? iparams : iz, r);
+    if (rc) return rc;
+    info->unit = r.unit;
+    info->variable = r.fixed_mode < 0 ? 1 : 0;
+    info->words_per_sample = r.words_per_sample;
+    info->min_seg_len = r.fixed_mode < 0 ? (var_lmin(r) + RS_RANGE_ALIGN - 1) / RS_RANGE_ALIGN * RS_RANGE_ALIGN
+                                         : RS_RANGE_ALIGN;
+    tally_seen(r, info->tally_seen);
+    info->pad = 0;
+    rs::clear_error();
+    return RS_OK;
+}
+
+rs_status rs_range_geometry(int32_t engine, int32_t dist, const double *fparams, const uint64_t *iparams,
+                            uint64_t words, uint64_t *seg_len, uint32_t *n_seg) {
+    std::lock_guard<std::mutex> g(g_mu);
+    double fz[4] = {0, 0, 0, 0};
+    u64 iz[4] = {0, 0, 0, 0};
+    Resolved r;
+    rs_status rc = resolve(dist, fparams ? fparams : fz, iparams ? iparams : iz, r);
+    if (rc) return rc;
+    if (r.fixed_mode >= 0 || is_serial(engine) || !rs_engine_supported(engine)) {
+        rs::set_error("range fills cover variable-consumption laws on skip-ahead engines");
+        return RS_ERR_UNSUPPORTED;
+    }
+    int dev;
+    CK(cudaGetDevice(&dev));
+    DevCtx *c;
+    if ((rc = init_dev(dev, &c))) return rc;
+    VarKernels K = var_kernels(engine, r.family);
+    int occ = std::min(occupancy(K.count), std::min(occupancy(K.fixup), occupancy(K.emit)));
+    u64 Tfull = (u64)c->sms * (u64)occ * BLOCK;  // one wave, as plan_segments
+    u64 L = (words + Tfull - 1) / Tfull;
+    if (L < var_lmin(r)) L = var_lmin(r);
+    L = (L + RS_RANGE_ALIGN - 1) / RS_RANGE_ALIGN * RS_RANGE_ALIGN;
+    u64 T = (words + L - 1) / L;
+    T = (T + BLOCK - 1) / BLOCK * BLOCK;
+    if (T < BLOCK) T = BLOCK;
+    if (T > 0xFFFFFFFFULL) { rs::set_error("slice too large"); return RS_ERR_VALUE; }
+    *seg_len = L;
+    *n_seg = (uint32_t)T;
+    rs::clear_error();
+    return RS_OK;
+}
+
+rs_status rs_range_count(const rs_stream *s, int32_t dist, const double *fparams, const uint64_t *iparams,
+                         uint64_t entry, uint64_t seg_len, uint32_t n_seg, rs_range_info *info, void *cuda_stream) {
+    std::lock_guard<std::mutex> g(g_mu);
+    rs_status rc = check_stream(s);
+    if (rc) return rc;
+    double fz[4] = {0, 0, 0, 0};
+    u64 iz[4] = {0, 0, 0, 0};
+    Resolved r;
+    if ((rc = resolve(dist, fparams ? fparams : fz, iparams ? iparams : iz, r))) return rc;
+    if (r.fixed_mode >= 0 || is_serial(s->engine)) {
+        rs::set_error("range fills cover variable-consumption laws on skip-ahead engines");
+        return RS_ERR_UNSUPPORTED;
+    }
+    if (s->cursor < s->fill || s->has_pending) {
+        rs::set_error("a range fill starts at a fresh stream position (no buffered words)");
+        return RS_ERR_VALUE;
+    }
+    if (seg_len == 0 || seg_len % RS_RANGE_ALIGN || n_seg == 0 || n_seg % BLOCK) {
+        rs::set_error("range geometry: seg_len must be a multiple of 72 and n_seg of 256");
+        return RS_ERR_VALUE;
+    }
+    const u64 u = (u64)r.unit;
+    if (entry >= u * seg_len) { rs::set_error("range entry beyond the first segment"); return RS_ERR_VALUE; }
+    int dev;
+    CK(cudaGetDevice(&dev));
+    DevCtx *c;
+    if ((rc = init_dev(dev, &c))) return rc;
+    c->range.valid = false;
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    FillPlan p;
+    memset(&p, 0, sizeof p);
+    fill_plan_common(p, *c, r, s->engine, s->full_mantissa);
+    memcpy(p.base, s->state, sizeof p.base);
+    memcpy(p.lanes, s->state, sizeof p.lanes);
+    p.lp0 = entry;
+    p.n = 0;
+    VarKernels K = var_kernels(s->engine, r.family);
+    const bool mem = parse_from_memory(s->engine);
+    if ((rc = plan_segments(*c, p, seg_len * n_seg, 0, 0, st, !mem, RS_RANGE_ALIGN, seg_len, n_seg))) return rc;
+    if ((rc = prep_chunk(*c, p, r, mem, st))) return rc;
+    CK(cudaMemsetAsync(c->res, 0, offsetof(DevResult, serial_state), st));
+    unsigned gdim = p.T / BLOCK;
+    int round = 0;
+    DevResult *res = c->res;
+    void *a1[] = {&p, &c->cnt0, &c->ex0, &c->cnt1, &c->ex1};
+    if ((rc = launch(K.count, dim3(gdim), dim3(BLOCK), a1, st))) return rc;
+    const u32 *prev = c->ex0;
+    u32 *ex_cur = c->exA, *ex_other = c->exB;
+    void *a2[] = {&p, &c->cnt0, &c->ex0, &c->cnt1, &c->ex1, &prev, &c->entry, &c->cnt, &ex_cur, &round, &res};
+    if ((rc = launch(K.fixup, dim3(gdim), dim3(BLOCK), a2, st))) return rc;
+    int rounds = 0;
+    for (;;) {  // entry resolution to a fixed point (as run_fill)
+        CK(cudaMemcpyAsync(c->res_host, c->res, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (!c->res_host->flag) break;
+        if (++round > (int)p.T) { rs::set_error("segment entry resolution did not converge"); return RS_ERR_INTERNAL; }
+        rounds++;
+        CK(cudaMemsetAsync(c->res, 0, offsetof(DevResult, serial_state), st));
+        prev = ex_cur;
+        void *a3[] = {&p, &c->cnt0, &c->ex0, &c->cnt1, &c->ex1, &prev, &c->entry, &c->cnt, &ex_other, &round, &res};
+        if ((rc = launch(K.fixup, dim3(gdim), dim3(BLOCK), a3, st))) return rc;
+        u32 *tmp = ex_cur; ex_cur = ex_other; ex_other = tmp;
+    }
+    size_t bytes = c->cub_bytes;
+    CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->cnt, c->off, (int)p.T, st));
+    u64 last_off = 0, last_cnt = 0;
+    u32 last_ex = 0;
+    CK(cudaMemcpyAsync(&last_off, c->off + (p.T - 1), 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&last_cnt, c->cnt + (p.T - 1), 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&last_ex, ex_cur + (p.T - 1), 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (mem) {
+        u32 over = 0, zero = 0;
+        CK(cudaMemcpy(&over, c->overrun, sizeof over, cudaMemcpyDeviceToHost));
+        if (over) {
+            CK(cudaMemcpy(c->overrun, &zero, sizeof zero, cudaMemcpyHostToDevice));
+            rs::set_error("parse ran past the materialized words (raise the slack)");
+            return RS_ERR_INTERNAL;
+        }
+    }
+    c->range.p = p;
+    c->range.K = K;
+    c->range.ex = ex_cur;
+    c->range.count = last_off + last_cnt;
+    c->range.unit = r.unit;
+    c->range.mem = mem;
+    c->range.valid = true;
+    if (info) {
+        memset(info, 0, sizeof *info);
+        info->count = last_off + last_cnt;
+        info->exit = last_ex;  // seg_end(T-1) == units(slice): the exit is past the slice end
+        info->end_pos = entry;
+        info->unit = r.unit;
+        info->resync_rounds = rounds;
+    }
+    rs::clear_error();
+    return RS_OK;
+}
+
+rs_status rs_range_emit(uint64_t keep, void *out_device, rs_range_info *info, void *cuda_stream) {
+    std::lock_guard<std::mutex> g(g_mu);
+    int dev;
+    CK(cudaGetDevice(&dev));
+    DevCtx *c;
+    rs_status rc;
+    if ((rc = init_dev(dev, &c))) return rc;
+    DevCtx::Range &R = c->range;
+    if (!R.valid) { rs::set_error("no counted range on this device (another fill ran in between?)"); return RS_ERR_VALUE; }
+    if (keep > R.count) { rs::set_error("keep exceeds the range's sample count"); return RS_ERR_VALUE; }
+    if (info) {
+        info->count = R.count;
+        info->end_pos = R.p.lp0;
+        for (int i = 0; i < 6; i++) info->tally[i] = 0;
+    }
+    if (keep == 0) { rs::clear_error(); return RS_OK; }
+    if (!out_device || !is_device_ptr(out_device)) { rs::set_error("range output must be device memory"); return RS_ERR_VALUE; }
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    FillPlan p = R.p;
+    p.n = keep;
+    p.out = out_device;
+    p.out0 = 0;
+    CK(cudaMemsetAsync(c->res, 0, offsetof(DevResult, serial_state), st));
+    DevResult *res = c->res;
+    void *a[] = {&p, &c->entry, &c->cnt, &c->off, &R.ex, &res};
+    if ((rc = launch(R.K.emit, dim3(p.T / BLOCK), dim3(BLOCK), a, st))) return rc;
+    CK(cudaMemcpyAsync(c->res_host, c->res, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    if (info) {
+        info->end_pos = c->res_host->end_pos;
+        for (int i = 0; i < 6; i++) info->tally[i] = c->res_host->tally[i];
+    }
     rs::clear_error();
     return RS_OK;
 }

@@ -476,3 +476,91 @@ def test_raw_bytes_device(engine):
     assert got == ref
     _assert_same_position(r, o)
     assert r.next_u64() == o.next_u64()
+
+
+# ----------------------------------------------------------------------------- multi-GPU sharding
+# World sizes simulated in one process on one GPU (the protocol's allgathers become
+# lists; each rank's slice runs through rs_range_count / rs_range_emit), checked against
+# the single-stream oracle fill: samples, final generator position and tallies.
+
+def _sim(engine, dist, params, n, world, seed=2024, **kw):
+    from oracle_ranges import simulate
+    from paper_2605_05099_b200 import shard
+
+    return simulate(lambda: state_io.create(engine, seed=[seed]), dist, params, n, world,
+                    lambda: shard.DeviceRanges(), **kw)
+
+
+SHARD_CASES = [
+    ("x256**", "norm", {}, 1 << 20, 8, {}),
+    ("pcg64", "norm", {}, 1 << 20, 3, {}),
+    ("x256++", "exp", {}, 1 << 19, 4, {}),
+    ("pcg64", "gamma", {"alpha": 2.5}, 1 << 18, 4, {}),
+    ("pcg64", "gamma", {"alpha": 0.3}, 1 << 17, 2, {}),
+    ("philox", "beta", {"a": 2.0, "b": 5.0}, 1 << 16, 3, {}),
+    ("ranlux++", "norm", {}, 1 << 18, 2, {}),
+    ("x256++simd", "norm", {}, 1 << 18, 4, {}),
+    ("pcg64", "uint64", {"b": (1 << 63) + 1}, 1 << 19, 4, {}),
+    ("x256**", "normf", {}, (1 << 19) + 1, 3, {}),
+    ("pcg64", "chi2", {"nu": 3.0}, 1 << 17, 2, {}),
+    ("x256**", "norm", {}, 1 << 18, 4, {"window": (72, 1)}),
+    ("pcg64", "gamma", {"alpha": 2.5}, 1 << 16, 3, {"window": (72, 1)}),
+    ("x256**", "norm", {}, 1 << 18, 2, {"words_per_rank": 1 << 16}),
+    ("x256**", "norm", {}, 0, 2, {}),
+]
+
+
+@pytest.mark.parametrize("engine,dist,params,n,world,kw", SHARD_CASES)
+def test_sharded_fill_vs_oracle(engine, dist, params, n, world, kw):
+    got, r, sfs = _sim(engine, dist, params, n, world, **kw)
+    o = O.OracleRng(engine, seed=[2024])
+    ref = o.fill(dist, params, n)
+    assert got.numel() == n
+    g = got.view(torch.int64).numpy() if got.dtype == torch.uint64 else got.numpy()
+    assert np.array_equal(_bits(g), _bits(ref))
+    _assert_same_position(r, o)
+    assert r.counters == o.tallies()
+    if n:
+        assert sum(sf.keep for sf in sfs) == n
+
+
+def test_sharded_fixed_consumption():
+    """Fixed-consumption laws shard by word offsets (u01f: two samples per word)."""
+    for engine, dist, n in (("philox", "u01f", (1 << 20) + 3), ("x256**", "uint64", 1 << 20), ("pcg64", "u01", 99999)):
+        got, r, sfs = _sim(engine, dist, {}, n, 3)
+        o = O.OracleRng(engine, seed=[2024])
+        ref = o.fill(dist, {}, n)
+        g = got.view(torch.int64).numpy() if got.dtype == torch.uint64 else got.numpy()
+        assert np.array_equal(_bits(g), _bits(ref)), engine
+        _assert_same_position(r, o)
+
+
+def test_fill_sharded_single_rank_and_errors():
+    from paper_2605_05099_b200 import shard
+
+    r = state_io.create("pcg64", seed=[99])
+    out, off = shard.fill_sharded(r, "gamma", {"alpha": 2.5}, 50000, 0, 1, lambda rec: [rec])
+    q = state_io.create("pcg64", seed=[99])
+    ref = q.fill("gamma", {"alpha": 2.5}, 50000)
+    assert off == 0 and torch.equal(out.view(torch.int64), ref.view(torch.int64))
+    assert r.get_state() == q.get_state() and r.buffer.cursor == q.buffer.cursor
+    with pytest.raises(ValueError):
+        shard.fill_sharded(r, "gamma", {"alpha": -1.0}, 10, 0, 1, lambda rec: [rec])
+    r.next_u64()  # mid-buffer: not a fresh position
+    with pytest.raises(ValueError):
+        shard.fill_sharded(r, "norm", {}, 10, 0, 1, lambda rec: [rec])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("engine,dist,params,n", [("x256**", "norm", {}, 1 << 28),
+                                                  ("pcg64", "gamma", {"alpha": 2.5}, 1 << 26),
+                                                  ("pcg64", "beta", {"a": 2.0, "b": 5.0}, 1 << 26)])
+def test_sharded_full_size_8_ranks(engine, dist, params, n):
+    """BASELINE sizes over 8 simulated ranks == the single-GPU fill (itself checked against
+    the oracle at these sizes above)."""
+    got, r, _ = _sim(engine, dist, params, n, 8, seed=99)
+    q = state_io.create(engine, seed=[99])
+    ref = q.fill(dist, params, n).cpu()
+    assert torch.equal(got.view(torch.int64), ref.view(torch.int64))
+    assert r.get_state() == q.get_state() and r.buffer.words == q.buffer.words and r.buffer.cursor == q.buffer.cursor
+    assert r.counters == q.counters

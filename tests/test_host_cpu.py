@@ -236,3 +236,18 @@ def test_default_engine_is_x256pp_simd():
     assert r.engine_id == "x256++simd"
     o = O.OracleRng("x256++simd", seed=[2024])
     assert r.get_state() == o.get_state()
+
+
+def test_dist_info_host_only():
+    """rs_dist_info needs no device: unit, variable-consumption flag and provisioning."""
+    from paper_2605_05099_b200 import shard
+
+    i = shard.dist_info(_lib.DIST_IDS["norm"], [0.0, 1.0], [])
+    assert (i.unit, i.variable, i.min_seg_len % 72) == (1, 1, 0) and 1.0 < i.words_per_sample < 1.1
+    assert list(i.tally_seen) == [1, 0, 0]
+    i = shard.dist_info(_lib.DIST_IDS["u01f"], [], [])
+    assert (i.unit, i.variable) == (2, 0)
+    i = shard.dist_info(_lib.DIST_IDS["gamma"], [2.5, 1.0], [])
+    assert i.variable == 1 and i.min_seg_len >= 1024 and list(i.tally_seen) == [1, 0, 1]
+    with pytest.raises(ValueError):
+        shard.dist_info(_lib.DIST_IDS["gamma"], [-1.0, 1.0], [])
