@@ -622,6 +622,10 @@ rs_status launch_raw_words(DevCtx &c, FillPlan &m, cudaStream_t st) {
 
 // shortest segment of a variable-consumption plan (gamma-family resync distances)
 u64 var_lmin(const Resolved &r) { return r.family == FAM_GAMMA ? (r.kind == GK_GAMMA ? 1024 : 2048) : 128; }
+// shortest segment of a range slice (multiple of RS_RANGE_ALIGN): a slice is 1/N of a fill,
+// so its segments are shorter than a whole fill's; resolution rounds absorb the rare
+// segment that a re-parse crosses without meeting its speculative parse
+u64 range_lmin(const Resolved &r) { return r.family == FAM_GAMMA ? 288 : 144; }
 
 // Per-chunk device inputs of the parse passes: the materialized engine words
 // (parse-from-memory engines) and the gamma family's boundary bitmaps.
@@ -1216,8 +1220,7 @@ rs_status rs_dist_info(int32_t dist, const double *fparams, const uint64_t *ipar
     info->unit = r.unit;
     info->variable = r.fixed_mode < 0 ? 1 : 0;
     info->words_per_sample = r.words_per_sample;
-    info->min_seg_len = r.fixed_mode < 0 ? (var_lmin(r) + RS_RANGE_ALIGN - 1) / RS_RANGE_ALIGN * RS_RANGE_ALIGN
-                                         : RS_RANGE_ALIGN;
+    info->min_seg_len = r.fixed_mode < 0 ? range_lmin(r) : RS_RANGE_ALIGN;
     tally_seen(r, info->tally_seen);
     info->pad = 0;
     rs::clear_error();
@@ -1244,7 +1247,7 @@ rs_status rs_range_geometry(int32_t engine, int32_t dist, const double *fparams,
     int occ = std::min(occupancy(K.count), std::min(occupancy(K.fixup), occupancy(K.emit)));
     u64 Tfull = (u64)c->sms * (u64)occ * BLOCK;  // one wave, as plan_segments
     u64 L = (words + Tfull - 1) / Tfull;
-    if (L < var_lmin(r)) L = var_lmin(r);
+    if (L < range_lmin(r)) L = range_lmin(r);
     L = (L + RS_RANGE_ALIGN - 1) / RS_RANGE_ALIGN * RS_RANGE_ALIGN;
     u64 T = (words + L - 1) / L;
     T = (T + BLOCK - 1) / BLOCK * BLOCK;

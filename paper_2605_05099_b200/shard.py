@@ -227,7 +227,7 @@ class ShardedFill:
         """Steps 1-2: entry guess from the warm-up window, then count + exit of the slice."""
         g = self.rank
         self.slice_rng = positioned(self.rng, g * self.R)
-        if g == 0 or self.n == 0:
+        if g == 0 or self.n == 0 or self.window[0] * self.window[1] == 0:  # (0, 0): no warm-up, guess 0
             self.entry = 0
         else:
             Lw, Tw = self.window

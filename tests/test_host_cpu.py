@@ -248,6 +248,6 @@ def test_dist_info_host_only():
     i = shard.dist_info(_lib.DIST_IDS["u01f"], [], [])
     assert (i.unit, i.variable) == (2, 0)
     i = shard.dist_info(_lib.DIST_IDS["gamma"], [2.5, 1.0], [])
-    assert i.variable == 1 and i.min_seg_len >= 1024 and list(i.tally_seen) == [1, 0, 1]
+    assert i.variable == 1 and i.min_seg_len >= 288 and list(i.tally_seen) == [1, 0, 1]
     with pytest.raises(ValueError):
         shard.dist_info(_lib.DIST_IDS["gamma"], [-1.0, 1.0], [])
