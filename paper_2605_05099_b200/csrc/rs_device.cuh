@@ -702,14 +702,20 @@ struct GammaPrm {
 // expression would; inside it (and for 0, NaN or f32-underflowing arguments, where
 // the comparisons fail) the exact det_log expression decides. This keeps the
 // ~10 % of attempts that miss the squeeze off the two-det_log divergent path.
-RS_DEV bool gamma_accept(double u, double zz, double v, const GammaPrm &g) {
+// the MUFU-log screen alone: +1 accept, -1 reject, 0 inside the band (the exact test decides)
+RS_DEV int gamma_screen(double u, double zz, double v, const GammaPrm &g) {
     double a = (double)__logf((float)u);
     double lv = (double)__logf((float)v);
     double b = 0.5 * zz + g.d - g.d * v + g.d * lv;
     double m = 1e-5 * (1.0 + fabs(a) + g.d * (1.0 + fabs(lv))) + 1e-12 * (zz + g.d * v);
-    if (a < b - m) return true;
-    if (a > b + m) return false;
+    return a < b - m ? 1 : (a > b + m ? -1 : 0);
+}
+RS_DEV bool gamma_exact(double u, double zz, double v, const GammaPrm &g) {  // continuous.py:199
     return det_log_dev(u) < 0.5 * zz + g.d - g.d * v + g.d * det_log_dev(v);
+}
+RS_DEV bool gamma_accept(double u, double zz, double v, const GammaPrm &g) {
+    int sc = gamma_screen(u, zz, v, g);
+    return sc != 0 ? sc > 0 : gamma_exact(u, zz, v, g);
 }
 
 template <class S>
@@ -1047,7 +1053,14 @@ struct DistGamma {  // continuous.py:183-212 (gamma, chi2 = gamma(nu/2, 2)), :21
         const double u = u01_of(uw, z.fm);
         const double zz = zn * zn;
         double val = g.td * v;
-        if (!(u < 1.0 - 0.0331 * zz * zz || gamma_accept(u, zz, v, g))) return false;
+        // The squeeze misses on ~10 % of attempts, so nearly every warp-step had a lane in
+        // the screen branch (and the accepted lanes then finished the step as two groups):
+        // the screen runs branch-free on every lane, only the in-band exact test branches.
+        const bool sq = u < 1.0 - 0.0331 * zz * zz;
+        const int sc = gamma_screen(u, zz, v, g);
+        bool acc = sq || sc > 0;
+        if (__builtin_expect(!sq && sc == 0, 0)) acc = gamma_exact(u, zz, v, g);
+        if (!acc) return false;
         if (g.boost) val = g.theta * val * det_exp_dev(det_log_dev(u01_of(s.next(), z.fm)) / g.alpha);
         if (kind == GK_GAMMA) {
             out = val;
