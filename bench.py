@@ -248,6 +248,9 @@ def run_ours(args, rank, world, local_rank):
     per_config = None
     if world == 1 and not args.no_per_config:
         per_config = run_per_config(dev, stream, sptr, out64, peak)
+    sharded = None
+    if world > 1 and not args.no_per_config:
+        sharded = run_sharded(rank, world, dev)
 
     traffic, limiter = None, None
     prof = os.path.join(ROOT, "profiles", "r01_ncu_philox_u01_f64.json")
@@ -282,7 +285,38 @@ def run_ours(args, rank, world, local_rank):
         line["e2e"] = e2e
     if per_config:
         line["per_config"] = per_config
+    if sharded:
+        line["sharded_c3"] = sharded
     return line
+
+
+def run_sharded(rank, world, dev, reps=3):
+    """C3 over N GPUs as ONE logical stream: x256** seed 2024 normals,
+    2^28 per GPU (weak), split by shard.fill_sharded -- warm-up entry guess, count, an
+    allgather of (entry, exit, count) per rank over NCCL, emit. Wall time per rank around
+    the whole protocol (it synchronises with the host), max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2605_05099_b200 import shard, state_io
+
+    n = (1 << 28) * world
+    gather = shard.torch_allgather()
+    best = None
+    for it in range(reps + 1):
+        r = state_io.create("x256**", seed=[2024])
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        out, off = shard.fill_sharded(r, "norm", {}, n, rank, world, gather)
+        torch.cuda.synchronize(dev)
+        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        del out
+        if it > 0:  # the first pass warms the plan caches
+            best = el.item() if best is None else min(best, el.item())
+    return {"workload": "x256** seed 2024 norm, 2^28 per GPU, one logical stream over %d ranks" % world,
+            "gsamples_s": n / best / 1e9, "ms": best * 1e3, "reps": reps,
+            "timing": "wall clock per rank around fill_sharded (host-synchronising protocol), max over ranks"}
 
 
 def run_per_config(dev, stream, sptr, buf, peak):
