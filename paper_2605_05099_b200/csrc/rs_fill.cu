@@ -64,6 +64,11 @@ struct DevCtx {
     u64 *words = nullptr;  // materialized engine words for parse-from-memory
     size_t words_bytes = 0;
     u32 *overrun = nullptr;  // device flag: a parse read past the materialized words
+    // gamma speculative store (FillPlan::spec ...): grown on demand
+    void *spec = nullptr;
+    size_t spec_bytes = 0;
+    void *pre = nullptr;
+    size_t pre_bytes = 0;
     // the counted slice of rs_range_count, waiting for rs_range_emit (its plan refers to
     // the scratch above, so any other fill on this device invalidates it)
     struct Range {
@@ -670,6 +675,36 @@ rs_status prep_chunk(DevCtx &c, FillPlan &p, const Resolved &r, bool mem, cudaSt
             c.bm_bytes = need;
         }
         p.bm = c.bm;
+    }
+    p.spec = nullptr;
+    if (r.family == FAM_GAMMA && r.kind == GK_GAMMA && !getenv("RS_NO_SPEC")) {
+        // an attempt draws 2 words, so a segment of L words starts <= L/2 + 1 samples
+        const u64 cap = (p.L / 2 + 8 + 3) / 4 * 4;
+        const size_t T = p.T;
+        size_t need = T * cap * 12;
+        if (need > c.spec_bytes) {
+            cudaFree(c.spec);
+            c.spec = nullptr;
+            CK(cudaMalloc(&c.spec, need));
+            c.spec_bytes = need;
+        }
+        size_t pneed = T * cap * 12 + T * 12 + 16;
+        if (pneed > c.pre_bytes) {
+            cudaFree(c.pre);
+            c.pre = nullptr;
+            CK(cudaMalloc(&c.pre, pneed));
+            c.pre_bytes = pneed;
+        }
+        p.spec_cap = cap;
+        p.spec = (double *)c.spec;
+        p.spec_tal = (u32 *)((char *)c.spec + T * cap * 8);
+        p.pre = (double *)c.pre;
+        p.pre_tal = (u32 *)((char *)c.pre + T * cap * 8);
+        p.cmode = p.pre_tal + T * cap;
+        p.pre_n = p.cmode + T;
+        p.spec_from = p.pre_n + T;
+        p.spec_over = p.spec_from + T;
+        CK(cudaMemsetAsync(p.spec_over, 0, 4, st));
     }
     return RS_OK;
 }

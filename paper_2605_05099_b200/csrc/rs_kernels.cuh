@@ -72,7 +72,26 @@ struct FillPlan {
     const u64 *rlx_A;
     void *out;
     u64 out0;                     // element index in `out` of this chunk's sample 0
+    // gamma (GK_GAMMA) speculative store: the count pass keeps its parse's samples (+ a
+    // packed per-sample tally word) per segment, the fixup keeps the re-parsed prefix, and
+    // the emit pass copies instead of parsing a third time
+    double *spec;                 // [T][spec_cap]
+    u32 *spec_tal;                // [T][spec_cap]
+    u64 spec_cap;
+    double *pre;                  // [T][spec_cap]: a prefix is at most a segment's samples
+    u32 *pre_tal;                 // [T][spec_cap]
+    u32 *cmode;                   // per segment: 1 = copy (pre + spec), 0 = re-parse
+    u32 *pre_n;                   // re-parsed prefix samples
+    u32 *spec_from;               // speculative sample index where the prefix meets it
+    u32 *spec_over;               // device flag: a segment or tally word overflowed (re-parse all)
 };
+// per-sample tally word of the gamma attempt machine: gamma attempts (8 bits), normal
+// attempts (12), normal pdf evaluations (12); 0xFFFFFFFF never occurs (flagged instead)
+__device__ __forceinline__ bool pack_tally(u32 ga, u32 na, u32 np, u32 &w) {
+    if (ga > 0xFF || na > 0xFFF || np > 0xFFF) return false;
+    w = ga | (na << 8) | (np << 20);
+    return true;
+}
 
 struct DevResult {
     u64 end_pos;     // logical position after the word that emitted sample n-1
@@ -516,6 +535,20 @@ __device__ __forceinline__ u64 bm_rank(const u32 *bm, u32 T, u32 t, u64 q) {
     for (u32 j = 0; j < k; j++) r += __popc(__ldg(&bm[(size_t)j * T + t]));
     return r + __popc(bm[(size_t)k * T + t] & ((1u << (q & 31)) - 1u));
 }
+// unit offset of the j-th recorded boundary (j = 0: the segment start), -1 if not recorded
+__device__ __forceinline__ long long bm_select(const u32 *bm, u32 T, u32 t, u32 W, u64 j) {
+    u64 r = 0;
+    for (u32 k = 0; k < W; k++) {
+        u32 w = __ldg(&bm[(size_t)k * T + t]);
+        u32 pc = __popc(w);
+        if (r + pc > j) {
+            for (u64 i = r; i < j; i++) w &= w - 1;  // drop the lower set bits
+            return 32LL * k + (__ffs(w) - 1);
+        }
+        r += pc;
+    }
+    return -1;
+}
 // bm_rank over bitmaps the calling thread wrote itself in this kernel (no __ldg)
 __device__ __forceinline__ u64 bm_rank_own(const u32 *bm, u32 T, u32 t, u64 q) {
     u32 k = (u32)(q >> 5);
@@ -542,7 +575,7 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_count(const __grid_consta
     make_src<E>(p, t, seg_start(p, t), s);
     typename DistOf<D>::type d;
     make_dist<D>(p, sm, d);
-    Tally tl;
+    Tally tl = {0, 0, 0, 0, 0};
     u64 c = 0;
     if constexpr (D == FAM_LEMIRE || D == FAM_U32) {  // independent one-unit tokens: unit-level loop
         bool bnd = true;
@@ -564,7 +597,34 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_count(const __grid_consta
             if constexpr (D == FAM_GAMMA) {
                 BmRec r{p.bm, p.T, t, seg_start(p, t), p.bmw};
                 r.put(r.start);  // phase 0 starts a sample at the segment start
-                if (d.am_applies()) {  // attempt-level machine (same samples and positions)
+                if (d.am_applies() && p.spec && d.kind == GK_GAMMA) {  // + speculative store
+                    __shared__ __align__(16) unsigned char ring_sp[128 * BLOCK];
+                    BatchRing<double, BLOCK> wv;
+                    BatchRing<u32, BLOCK> wt;
+                    wv.init(p.spec, (u64)t * p.spec_cap, (double *)ring_sp + threadIdx.x);
+                    wt.init(p.spec_tal, (u64)t * p.spec_cap, (u32 *)(ring_sp + 64 * BLOCK) + threadIdx.x);
+                    GammaAM m{0, 0, 0.0};
+                    Tally t0 = tl;
+                    bool over = false;
+                    u32 it = 0;
+                    while (true) {
+                        double v;
+                        if (d.am_step(m, s, tl, v)) {
+                            c++;
+                            r.put(s.pos);
+                            u32 w;
+                            over |= !pack_tally(tl.gamma_att - t0.gamma_att, tl.norm_att - t0.norm_att,
+                                                tl.norm_pdf - t0.norm_pdf, w);
+                            t0 = tl;
+                            if (c <= p.spec_cap) { wv.put(v); wt.put(w); }
+                            if (s.pos >= end) break;
+                        }
+                        if ((++it & 3) == 0) { wv.tick(); wt.tick(); }
+                    }
+                    wv.finish();
+                    wt.finish();
+                    if (over || c > p.spec_cap) atomicOr(p.spec_over, 1u);
+                } else if (d.am_applies()) {  // attempt-level machine (same samples and positions)
                     GammaAM m{0, 0, 0.0};
                     while (true) {
                         double v;
@@ -654,8 +714,11 @@ __device__ void resolve_entry(const FillPlan &p, const ZigFast *sm, u32 t, u32 e
             make_src<E>(p, t, start + e, sb);
             typename DistOf<D>::type d;
             make_dist<D>(p, sm, d);
-            Tally tl;
+            Tally tl = {0, 0, 0, 0, 0};
             const bool two = d.paired();
+            // speculative store (GK_GAMMA): keep the prefix samples for k_emit's copy
+            const bool sp = p.spec && d.kind == GK_GAMMA && d.am_applies();
+            bool keep = sp;
             const u32 *bm0 = p.bm, *bm1 = p.bm + (size_t)p.bmw * p.T;
             u64 nb = 0;
             u32 kw = ~0u, wa = 0, wc = 0;
@@ -663,6 +726,7 @@ __device__ void resolve_entry(const FillPlan &p, const ZigFast *sm, u32 t, u32 e
                 if (sb.pos >= end) {
                     cnt = nb;
                     ex = (u32)(sb.pos - end);
+                    if (sp) { p.cmode[t] = keep; p.pre_n[t] = (u32)nb; p.spec_from[t] = 0; }
                     return;
                 }
                 u64 q = sb.pos - start;
@@ -674,8 +738,10 @@ __device__ void resolve_entry(const FillPlan &p, const ZigFast *sm, u32 t, u32 e
                     if (two) wc = bm1[(size_t)k * p.T + t];
                 }
                 if (wa & bit) {
-                    cnt = c0 - bm_rank(bm0, p.T, t, q) + nb;
+                    const u64 rk = bm_rank(bm0, p.T, t, q);
+                    cnt = c0 - rk + nb;
                     ex = x0;
+                    if (sp) { p.cmode[t] = keep; p.pre_n[t] = (u32)nb; p.spec_from[t] = (u32)rk; }
                     return;
                 }
                 if (two && (wc & bit)) {
@@ -686,12 +752,24 @@ __device__ void resolve_entry(const FillPlan &p, const ZigFast *sm, u32 t, u32 e
                 if (d.am_applies()) {  // one sample through the attempt-level machine
                     GammaAM m{0, 0, 0.0};
                     double v;
+                    Tally t0 = tl;
                     while (!d.am_step(m, sb, tl, v)) {}
+                    if (keep) {
+                        u32 w;
+                        if (nb < p.spec_cap && pack_tally(tl.gamma_att - t0.gamma_att, tl.norm_att - t0.norm_att,
+                                                       tl.norm_pdf - t0.norm_pdf, w)) {
+                            p.pre[(size_t)t * p.spec_cap + nb] = v;
+                            p.pre_tal[(size_t)t * p.spec_cap + nb] = w;
+                        } else {
+                            keep = false;
+                        }
+                    }
                 } else {
                     d.sample(sb, tl);
                 }
                 nb++;
             }
+            if (sp) p.cmode[t] = 0;
         }  // no meeting in the recorded window: the lockstep parse below
     }
     typename SrcOf<E, D>::type sa, sb, sc;
@@ -699,7 +777,7 @@ __device__ void resolve_entry(const FillPlan &p, const ZigFast *sm, u32 t, u32 e
     make_src<E>(p, t, start + e, sb);
     typename DistOf<D>::type d;
     make_dist<D>(p, sm, d);
-    Tally tl;
+    Tally tl = {0, 0, 0, 0, 0};
     const bool two = d.paired();
     if (two) {  // the phase-1 parse: lone second sub-sample first
         make_src<E>(p, t, start, sc);
@@ -758,6 +836,7 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_fixup(const __grid_consta
     if (e == 0) {
         c = cnt0[t];
         x = ex0[t];
+        if (p.spec) { p.cmode[t] = 1; p.pre_n[t] = 0; p.spec_from[t] = 0; }
     } else {
         resolve_entry<E, D>(p, sm, t, e, cnt0[t], ex0[t], cnt1[t], ex1[t], c, x);
     }
@@ -776,13 +855,69 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constan
     stage_tables(p, sm);
     u32 t = blockIdx.x * BLOCK + threadIdx.x;
     Tally tl = {0, 0, 0, 0, 0};
+    bool cp = false;
+    if constexpr (D == FAM_GAMMA) {
+        // Speculative store (GK_GAMMA): a segment whose samples are the count pass's (after
+        // the fixup's re-parsed prefix) is copied, not parsed; the one holding sample n-1
+        // still re-parses (it reports the end position). The copy is warp-cooperative:
+        // the warp walks its lanes' runs with coalesced 256-byte loads and stores.
+        if (p.spec && p.kind == GK_GAMMA && !*p.spec_over) {
+            const u32 lane = threadIdx.x & 31;
+            u64 o = 0, c = 0, endp = 0;
+            if (t < p.T) {
+                o = off[t];
+                c = cnt[t];
+                cp = o < p.n && c > 0 && p.cmode[t];
+                if (cp && o + c >= p.n) {  // holds sample n-1: the position after it
+                    if (o + c == p.n) {
+                        endp = seg_end(p, t) + ex[t];
+                    } else {  // = the start of the next speculative sample, from the boundary bitmap
+                        const u64 kk = p.n - o - 1, pn = p.pre_n[t];
+                        long long q = kk < pn ? -1 : bm_select(p.bm, p.T, t, p.bmw, p.spec_from[t] + (kk - pn) + 1);
+                        if (q < 0) cp = false;
+                        else endp = seg_start(p, t) + (u64)q;
+                    }
+                }
+            }
+            unsigned m = __ballot_sync(0xFFFFFFFFu, cp);
+            while (m) {
+                const int j = __ffs(m) - 1;
+                m &= m - 1;
+                const u32 tj = t - lane + j;
+                const u64 oj = __shfl_sync(0xFFFFFFFFu, o, j), c0j = __shfl_sync(0xFFFFFFFFu, c, j);
+                const u64 endj = __shfl_sync(0xFFFFFFFFu, endp, j);
+                const u64 cj = c0j < p.n - oj ? c0j : p.n - oj;
+                const u64 pn = p.pre_n[tj];
+                const size_t pb = (size_t)tj * p.spec_cap;
+                const size_t sb = (size_t)tj * p.spec_cap + p.spec_from[tj] - pn;  // + k for k >= pn
+                double *dst = (double *)p.out + p.out0 + oj;
+#pragma unroll 4
+                for (u64 k = lane; k < cj; k += 32) {
+                    double v;
+                    u32 w;
+                    if (k < pn) {
+                        v = p.pre[pb + k];
+                        w = p.pre_tal[pb + k];
+                    } else {
+                        v = __ldg(p.spec + (sb + k));
+                        w = __ldg(p.spec_tal + (sb + k));
+                    }
+                    dst[k] = v;
+                    tl.gamma_att += w & 0xFF;
+                    tl.norm_att += (w >> 8) & 0xFFF;
+                    tl.norm_pdf += w >> 20;
+                }
+                if (lane == 0 && oj + cj == p.n) res->end_pos = endj;
+            }
+        }
+    }
     if (t < p.T) {
         u64 o = off[t], c = cnt[t];
         if (t == p.T - 1) {
             res->total = o + c;
             res->next_start = seg_end(p, t) + ex[t];
         }
-        if (o < p.n && c > 0) {
+        if (o < p.n && c > 0 && !cp) {
             u64 kmax = c < p.n - o ? c : p.n - o;
             typename SrcOf<E, D>::type s;
             make_src<E>(p, t, seg_start(p, t) + entry[t], s);
@@ -1463,7 +1598,7 @@ __global__ void __launch_bounds__(STR_BLOCK) k_streams(const __grid_constant__ S
     DistArgs da{a.fp, a.ip, &a.ga, &a.gb, a.kind, a.fm, a.zslow, a.zslowf};
     make_dist_a<(D == FAM_FIXED || D == FAM_LEMIRE_RING) ? FAM_LEMIRE : D>(da, sm, d);
     typedef typename DT::out_t T;
-    Tally tl;
+    Tally tl = {0, 0, 0, 0, 0};
     if constexpr (sizeof(T) == 8) {
         if (tiled) {
             if constexpr (D == FAM_LEMIRE_RING) {

@@ -283,8 +283,8 @@ class ShardedFill:
             self.out = torch.cat([self.out, tail.to(self.out.device)])
             self.keep += int(tail.numel())
             rec = [2, 0] + [a + b for a, b in zip(self.tally, tal)]
-            rec += list(t.engine.s) + [len(t.buffer.words), t.buffer.cursor,
-                                       -1 if t.buffer.pending is None else t.buffer.pending] + list(t.buffer.words)
+            rec += list(t.engine.s) + [len(t.buffer.words), t.buffer.cursor, 0 if t.buffer.pending is None else 1,
+                                       t.buffer.pending or 0] + list(t.buffer.words)
         return rec
 
     def finish(self, table):
@@ -303,10 +303,10 @@ class ShardedFill:
             t = tails[0][8:]
             sw = r.engine.STATE_WORDS
             r.engine.s = [int(v) for v in t[:sw]]
-            nbuf, cur, pend = int(t[sw]), int(t[sw + 1]), int(t[sw + 2])
-            r.buffer.words = [int(v) for v in t[sw + 3:sw + 3 + nbuf]]
+            nbuf, cur, has, pend = int(t[sw]), int(t[sw + 1]), int(t[sw + 2]), int(t[sw + 3])
+            r.buffer.words = [int(v) for v in t[sw + 4:sw + 4 + nbuf]]
             r.buffer.cursor = cur
-            r.buffer.pending = None if pend < 0 else pend
+            r.buffer.pending = pend if has else None
             return
         ends = [(h, t[1]) for h, t in enumerate(table) if t[0] == 1]
         if not ends:  # n == 0: nothing consumed
@@ -365,13 +365,24 @@ def fill_sharded(rng, dist, params, n, rank, world, allgather, ranges=None, word
     return sf.out, off
 
 
-def torch_allgather(group=None):
-    """allgather over torch.distributed (NCCL or gloo): a few integers per rank."""
+def torch_allgather(group=None, width=256):
+    """allgather over torch.distributed (NCCL or gloo): each rank's record is a few
+    integers (at most `width`, u64 values as their int64 bit patterns), sent as one
+    fixed-size int64 tensor on the rank's device (NCCL) or host (gloo)."""
     import torch.distributed as dist
 
     def gather(rec):
-        objs = [None] * dist.get_world_size(group)
-        dist.all_gather_object(objs, [int(v) for v in rec], group=group)
-        return objs
+        rec = [int(v) for v in rec]
+        if len(rec) + 1 > width:
+            raise ValueError("allgather record longer than %d words" % width)
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+        row = [len(rec)] + [v - (1 << 64) if v >= (1 << 63) else v for v in rec]
+        t = torch.zeros(width, dtype=torch.int64, device=dev)
+        t[:len(row)] = torch.tensor(row, dtype=torch.int64)
+        world = dist.get_world_size(group)
+        parts = [torch.empty(width, dtype=torch.int64, device=dev) for _ in range(world)]
+        dist.all_gather(parts, t, group=group)
+        rows = torch.stack(parts).cpu().tolist()
+        return [[v & 0xFFFFFFFFFFFFFFFF if v < 0 else v for v in r[1:1 + r[0]]] for r in rows]
 
     return gather
