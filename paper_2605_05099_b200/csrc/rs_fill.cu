@@ -677,18 +677,20 @@ rs_status prep_chunk(DevCtx &c, FillPlan &p, const Resolved &r, bool mem, cudaSt
         p.bm = c.bm;
     }
     p.spec = nullptr;
-    if (r.family == FAM_GAMMA && r.kind == GK_GAMMA && !getenv("RS_NO_SPEC")) {
+    if (r.family == FAM_GAMMA && r.kind != GK_T && !getenv("RS_NO_SPEC")) {
         // an attempt draws 2 words, so a segment of L words starts <= L/2 + 1 samples
-        const u64 cap = (p.L / 2 + 8 + 3) / 4 * 4;
+        // (<= L/4 + 1 for the paired laws: two gamma sub-samples per sample)
+        const bool paired = r.kind != GK_GAMMA;
+        const u64 cap = (p.L / (paired ? 4 : 2) + 8 + 3) / 4 * 4;
         const size_t T = p.T;
-        size_t need = T * cap * 12;
+        size_t need = T * cap * 12 * (paired ? 2 : 1);
         if (need > c.spec_bytes) {
             cudaFree(c.spec);
             c.spec = nullptr;
             CK(cudaMalloc(&c.spec, need));
             c.spec_bytes = need;
         }
-        size_t pneed = T * cap * 12 + T * 12 + 16;
+        size_t pneed = T * cap * 12 + T * 20 + 16;
         if (pneed > c.pre_bytes) {
             cudaFree(c.pre);
             c.pre = nullptr;
@@ -703,7 +705,11 @@ rs_status prep_chunk(DevCtx &c, FillPlan &p, const Resolved &r, bool mem, cudaSt
         p.cmode = p.pre_tal + T * cap;
         p.pre_n = p.cmode + T;
         p.spec_from = p.pre_n + T;
-        p.spec_over = p.spec_from + T;
+        p.c1own = p.spec_from + T;
+        p.mrank0 = p.c1own + T;
+        p.spec_over = p.mrank0 + T;
+        p.spec1 = paired ? (double *)((char *)c.spec + T * cap * 12) : nullptr;
+        p.spec1_tal = paired ? (u32 *)((char *)c.spec + T * cap * 20) : nullptr;
         CK(cudaMemsetAsync(p.spec_over, 0, 4, st));
     }
     return RS_OK;

@@ -84,6 +84,11 @@ struct FillPlan {
     u32 *pre_n;                   // re-parsed prefix samples
     u32 *spec_from;               // speculative sample index where the prefix meets it
     u32 *spec_over;               // device flag: a segment or tally word overflowed (re-parse all)
+    // paired laws (beta, F): the phase-1 parse's own samples (before it merges with phase 0)
+    double *spec1;                // [T][spec_cap]
+    u32 *spec1_tal;               // [T][spec_cap]
+    u32 *c1own;                   // phase-1 samples before the merge (all of them if none)
+    u32 *mrank0;                  // phase-0 sample index at the merge point
 };
 // per-sample tally word of the gamma attempt machine: gamma attempts (8 bits), normal
 // attempts (12), normal pdf evaluations (12); 0xFFFFFFFF never occurs (flagged instead)
@@ -557,6 +562,86 @@ __device__ __forceinline__ u64 bm_rank_own(const u32 *bm, u32 T, u32 t, u64 q) {
     for (u32 j = 0; j < k; j++) r += __popc(bm[(size_t)j * T + t]);
     return r + __popc(bm[(size_t)k * T + t] & ((1u << (q & 31)) - 1u));
 }
+// The count pass's phase-1 parse of a paired law (kept out of line: its registers and
+// its speculative store would otherwise weigh on the phase-0 loop of every gamma law).
+template <int E, int D>
+__device__ __noinline__ void count_phase1(const FillPlan &p, const typename DistOf<D>::type &d, u32 t, u64 end,
+                                          u64 c, u64 spos, Tally &tl, unsigned char *ring_sp, u64 *cnt1,
+                                          u32 *ex1) {
+        typename SrcOf<E, D>::type s1;
+        make_src<E>(p, t, seg_start(p, t), s1);
+        u64 c1 = 0;
+        BmRec r{p.bm ? p.bm + (size_t)p.bmw * p.T : nullptr, p.T, t, seg_start(p, t), p.bmw};
+        bool am = false;
+        if constexpr (D == FAM_GAMMA) am = d.am_applies();
+        bool merged = false;
+        if (am) {
+            if constexpr (D == FAM_GAMMA) {
+                GammaAM m{1, 1, 0.0};  // a lone second sub-sample first
+                double v;
+                while (!d.am_step(m, s1, tl, v)) {}
+                r.put(s1.pos);  // phase 1's first full sample starts after the lone second
+                // speculative store of phase 1's own samples (the rest are phase 0's)
+                const bool sp = p.spec != nullptr;
+                BatchRing<double, BLOCK> wv;
+                BatchRing<u32, BLOCK> wt;
+                if (sp) {
+                    wv.init(p.spec1, (u64)t * p.spec_cap, (double *)ring_sp + threadIdx.x);
+                    wt.init(p.spec1_tal, (u64)t * p.spec_cap, (u32 *)(ring_sp + 64 * BLOCK) + threadIdx.x);
+                }
+                Tally t0 = tl;
+                bool over = false;
+                u32 it = 0;
+                u64 rk0 = 0;
+                // Once phase 1 starts a sample where phase 0 did, the two parses coincide
+                // to the segment end: the rest of phase 1's count is phase 0's, read off
+                // the phase-0 bitmap this thread just wrote (plain loads: own stores).
+                const u32 *b0 = p.bm;
+                const u64 st0 = seg_start(p, t);
+                while (s1.pos < end) {
+                    if (b0) {
+                        const u64 q = s1.pos - st0;
+                        if ((b0[(size_t)(q >> 5) * p.T + t] >> (q & 31)) & 1) {
+                            rk0 = bm_rank_own(b0, p.T, t, q);
+                            merged = true;
+                            break;
+                        }
+                    }
+                    while (!d.am_step(m, s1, tl, v)) {}
+                    c1++;
+                    r.put(s1.pos);
+                    if (sp) {
+                        u32 w;
+                        over |= !pack_tally(tl.gamma_att - t0.gamma_att, tl.norm_att - t0.norm_att,
+                                            tl.norm_pdf - t0.norm_pdf, w);
+                        t0 = tl;
+                        if (c1 <= p.spec_cap) { wv.put(v); wt.put(w); }
+                        if ((++it & 3) == 0) { wv.tick(); wt.tick(); }
+                    }
+                }
+                if (sp) {
+                    wv.finish();
+                    wt.finish();
+                    if (over || c1 > p.spec_cap) atomicOr(p.spec_over, 1u);
+                    p.c1own[t] = (u32)c1;
+                    p.mrank0[t] = (u32)rk0;
+                }
+                if (merged) c1 += c - rk0;
+            }
+        } else {
+            d.skip_second(s1, tl);
+            r.put(s1.pos);  // phase 1's first full sample starts after the lone second
+            while (s1.pos < end) {
+                d.sample(s1, tl);
+                c1++;
+                r.put(s1.pos);
+            }
+        }
+        r.close();
+        cnt1[t] = c1;
+        ex1[t] = merged ? (u32)(spos - end) : (u32)(s1.pos - end);
+}
+
 // count: samples that START inside [seg_start, seg_end) and the exit (first sample
 // boundary at or beyond seg_end), parsing from seg_start as if it were a boundary.
 // For paired samplers (beta, f, t, skew_normal: two sub-samples per sample) a parse
@@ -567,6 +652,7 @@ template <int E, int D>
 __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_count(const __grid_constant__ FillPlan p, u64 *cnt0, u32 *ex0,
                                                             u64 *cnt1, u32 *ex1) {
     __shared__ ZigFast sm[256];
+    __shared__ __align__(16) unsigned char ring_sp[D == FAM_GAMMA ? 128 * BLOCK : 16];  // speculative store
     stage_tables(p, sm);
     u32 t = blockIdx.x * BLOCK + threadIdx.x;
     if (t >= p.T) return;
@@ -597,8 +683,7 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_count(const __grid_consta
             if constexpr (D == FAM_GAMMA) {
                 BmRec r{p.bm, p.T, t, seg_start(p, t), p.bmw};
                 r.put(r.start);  // phase 0 starts a sample at the segment start
-                if (d.am_applies() && p.spec && d.kind == GK_GAMMA) {  // + speculative store
-                    __shared__ __align__(16) unsigned char ring_sp[128 * BLOCK];
+                if (d.am_applies() && p.spec) {  // + speculative store
                     BatchRing<double, BLOCK> wv;
                     BatchRing<u32, BLOCK> wt;
                     wv.init(p.spec, (u64)t * p.spec_cap, (double *)ring_sp + threadIdx.x);
@@ -649,52 +734,7 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_count(const __grid_consta
                 }
             }
         }
-        if (d.paired()) {
-            typename SrcOf<E, D>::type s1;
-            make_src<E>(p, t, seg_start(p, t), s1);
-            u64 c1 = 0;
-            BmRec r{p.bm ? p.bm + (size_t)p.bmw * p.T : nullptr, p.T, t, seg_start(p, t), p.bmw};
-            bool am = false;
-            if constexpr (D == FAM_GAMMA) am = d.am_applies();
-            bool merged = false;
-            if (am) {
-                if constexpr (D == FAM_GAMMA) {
-                    GammaAM m{1, 1, 0.0};  // a lone second sub-sample first
-                    double v;
-                    while (!d.am_step(m, s1, tl, v)) {}
-                    r.put(s1.pos);  // phase 1's first full sample starts after the lone second
-                    // Once phase 1 starts a sample where phase 0 did, the two parses coincide
-                    // to the segment end: the rest of phase 1's count is phase 0's, read off
-                    // the phase-0 bitmap this thread just wrote (plain loads: own stores).
-                    const u32 *b0 = p.bm;
-                    const u64 st0 = seg_start(p, t);
-                    while (s1.pos < end) {
-                        if (b0) {
-                            const u64 q = s1.pos - st0;
-                            if ((b0[(size_t)(q >> 5) * p.T + t] >> (q & 31)) & 1) {
-                                c1 += c - bm_rank_own(b0, p.T, t, q);
-                                merged = true;
-                                break;
-                            }
-                        }
-                        while (!d.am_step(m, s1, tl, v)) {}
-                        c1++;
-                        r.put(s1.pos);
-                    }
-                }
-            } else {
-                d.skip_second(s1, tl);
-                r.put(s1.pos);  // phase 1's first full sample starts after the lone second
-                while (s1.pos < end) {
-                    d.sample(s1, tl);
-                    c1++;
-                    r.put(s1.pos);
-                }
-            }
-            r.close();
-            cnt1[t] = c1;
-            ex1[t] = merged ? (u32)(s.pos - end) : (u32)(s1.pos - end);
-        }
+        if (d.paired()) count_phase1<E, D>(p, d, t, end, c, s.pos, tl, ring_sp, cnt1, ex1);
     }
     cnt0[t] = c;
     ex0[t] = (u32)(s.pos - end);
@@ -717,7 +757,7 @@ __device__ void resolve_entry(const FillPlan &p, const ZigFast *sm, u32 t, u32 e
             Tally tl = {0, 0, 0, 0, 0};
             const bool two = d.paired();
             // speculative store (GK_GAMMA): keep the prefix samples for k_emit's copy
-            const bool sp = p.spec && d.kind == GK_GAMMA && d.am_applies();
+            const bool sp = p.spec && d.am_applies();
             bool keep = sp;
             const u32 *bm0 = p.bm, *bm1 = p.bm + (size_t)p.bmw * p.T;
             u64 nb = 0;
@@ -745,8 +785,10 @@ __device__ void resolve_entry(const FillPlan &p, const ZigFast *sm, u32 t, u32 e
                     return;
                 }
                 if (two && (wc & bit)) {
-                    cnt = c1 - bm_rank(bm1, p.T, t, q) + nb;
+                    const u64 rk = bm_rank(bm1, p.T, t, q);
+                    cnt = c1 - rk + nb;
                     ex = x1;
+                    if (sp) { p.cmode[t] = keep ? 2u : 0u; p.pre_n[t] = (u32)nb; p.spec_from[t] = (u32)rk; }
                     return;
                 }
                 if (d.am_applies()) {  // one sample through the attempt-level machine
@@ -861,7 +903,7 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constan
         // the fixup's re-parsed prefix) is copied, not parsed; the one holding sample n-1
         // still re-parses (it reports the end position). The copy is warp-cooperative:
         // the warp walks its lanes' runs with coalesced 256-byte loads and stores.
-        if (p.spec && p.kind == GK_GAMMA && !*p.spec_over) {
+        if (p.spec && p.kind != GK_T && !*p.spec_over) {
             const u32 lane = threadIdx.x & 31;
             u64 o = 0, c = 0, endp = 0;
             if (t < p.T) {
@@ -871,9 +913,21 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constan
                 if (cp && o + c >= p.n) {  // holds sample n-1: the position after it
                     if (o + c == p.n) {
                         endp = seg_end(p, t) + ex[t];
-                    } else {  // = the start of the next speculative sample, from the boundary bitmap
+                    } else {  // = the start of the next speculative sample, from the boundary bitmaps
                         const u64 kk = p.n - o - 1, pn = p.pre_n[t];
-                        long long q = kk < pn ? -1 : bm_select(p.bm, p.T, t, p.bmw, p.spec_from[t] + (kk - pn) + 1);
+                        long long q = -1;
+                        if (kk >= pn) {
+                            const u64 i = p.spec_from[t] + (kk - pn);  // speculative index of sample n-1
+                            const u32 *bm1 = p.bm + (size_t)p.bmw * p.T;
+                            if (p.cmode[t] == 1) {
+                                q = bm_select(p.bm, p.T, t, p.bmw, i + 1);
+                            } else {
+                                const u64 own = p.c1own[t];
+                                if (i + 1 < own) q = bm_select(bm1, p.T, t, p.bmw, i + 1);
+                                else if (i + 1 == own) q = bm_select(p.bm, p.T, t, p.bmw, p.mrank0[t]);
+                                else q = bm_select(p.bm, p.T, t, p.bmw, p.mrank0[t] + (i - own) + 1);
+                            }
+                        }
                         if (q < 0) cp = false;
                         else endp = seg_start(p, t) + (u64)q;
                     }
@@ -887,26 +941,38 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constan
                 const u64 oj = __shfl_sync(0xFFFFFFFFu, o, j), c0j = __shfl_sync(0xFFFFFFFFu, c, j);
                 const u64 endj = __shfl_sync(0xFFFFFFFFu, endp, j);
                 const u64 cj = c0j < p.n - oj ? c0j : p.n - oj;
-                const u64 pn = p.pre_n[tj];
-                const size_t pb = (size_t)tj * p.spec_cap;
-                const size_t sb = (size_t)tj * p.spec_cap + p.spec_from[tj] - pn;  // + k for k >= pn
+                const u64 pn = p.pre_n[tj] < cj ? p.pre_n[tj] : cj;
+                const u64 sf = p.spec_from[tj];
+                const size_t row = (size_t)tj * p.spec_cap;
                 double *dst = (double *)p.out + p.out0 + oj;
-#pragma unroll 4
-                for (u64 k = lane; k < cj; k += 32) {
-                    double v;
-                    u32 w;
-                    if (k < pn) {
-                        v = p.pre[pb + k];
-                        w = p.pre_tal[pb + k];
-                    } else {
-                        v = __ldg(p.spec + (sb + k));
-                        w = __ldg(p.spec_tal + (sb + k));
-                    }
-                    dst[k] = v;
-                    tl.gamma_att += w & 0xFF;
-                    tl.norm_att += (w >> 8) & 0xFFF;
-                    tl.norm_pdf += w >> 20;
+                // up to three contiguous pieces: the re-parsed prefix, the speculative run it met
+                // (phase 0, or phase 1 up to its merge), then phase 0 from the merge point
+                u64 ka = cj;  // end of the second piece
+                const double *va = p.spec + row + sf;
+                const u32 *wa = p.spec_tal + row + sf;
+                const double *vb = nullptr;
+                const u32 *wb = nullptr;
+                if (p.cmode[tj] == 2) {
+                    va = p.spec1 + row + sf;
+                    wa = p.spec1_tal + row + sf;
+                    const u64 kown = pn + p.c1own[tj] - sf;
+                    if (kown < cj) ka = kown;
+                    vb = p.spec + row + p.mrank0[tj];
+                    wb = p.spec_tal + row + p.mrank0[tj];
                 }
+                auto piece = [&](const double *v, const u32 *w, u64 k0, u64 k1) {
+#pragma unroll 4
+                    for (u64 k = k0 + lane; k < k1; k += 32) {
+                        const u32 x = __ldg(w + (k - k0));
+                        dst[k] = __ldg(v + (k - k0));
+                        tl.gamma_att += x & 0xFF;
+                        tl.norm_att += (x >> 8) & 0xFFF;
+                        tl.norm_pdf += x >> 20;
+                    }
+                };
+                piece(p.pre + row, p.pre_tal + row, 0, pn);
+                piece(va, wa, pn, ka);
+                if (vb) piece(vb, wb, ka, cj);
                 if (lane == 0 && oj + cj == p.n) res->end_pos = endj;
             }
         }
