@@ -565,3 +565,22 @@ def test_sharded_full_size_8_ranks(engine, dist, params, n):
     assert torch.equal(got.view(torch.int64), ref.view(torch.int64))
     assert r.get_state() == q.get_state() and r.buffer.words == q.buffer.words and r.buffer.cursor == q.buffer.cursor
     assert r.counters == q.counters
+
+
+@pytest.mark.parametrize("dist,params,n", [("gamma", {"alpha": 2.5}, 1 << 20), ("beta", {"a": 2.0, "b": 5.0}, 1 << 19),
+                                           ("gamma", {"alpha": 0.3}, 1 << 19), ("f", {"nu1": 3.0, "nu2": 7.0}, 1 << 18)])
+def test_gamma_family_with_and_without_speculative_store(monkeypatch, dist, params, n):
+    """The gamma family's emit copies the count pass's stored samples (DESIGN 4.5b);
+    RS_NO_SPEC=1 selects the three-parse path. Both equal the oracle, tallies included."""
+    o = O.OracleRng("pcg64", seed=[5])
+    ref = o.fill(dist, params, n)
+    for flag in (None, "1"):
+        if flag:
+            monkeypatch.setenv("RS_NO_SPEC", flag)
+        else:
+            monkeypatch.delenv("RS_NO_SPEC", raising=False)
+        r = state_io.create("pcg64", seed=[5])
+        got = r.fill(dist, params, n).cpu().numpy()
+        assert np.array_equal(_bits(got), _bits(ref)), flag
+        _assert_same_position(r, o, str(flag))
+        assert r.counters == o.tallies()
