@@ -404,7 +404,27 @@ def run_per_config(dev, stream, sptr, buf, peak):
         el = time.perf_counter() - t0
         res["c5a_mvn_d%d_2p20" % d] = {"vectors_per_s": (1 << 20) / el, "ms": el * 1e3,
                                         "gflops_dense": 2.0 * (1 << 20) * d * d / el / 1e9,
+                                        "gflops_triangular": 1.0 * (1 << 20) * d * (d + 1) / el / 1e9,
                                         "note": "wall clock incl. host Cholesky and sync (rs_mvn is synchronous)"}
+    # FP64 peak for the MVN contraction: cuBLAS DGEMM 8192^3 through torch
+    m = 8192
+    a64 = torch.randn(m, m, dtype=torch.float64, device=dev)
+    b64 = torch.randn(m, m, dtype=torch.float64, device=dev)
+    c64 = torch.matmul(a64, b64)
+    best = 1e9
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        torch.matmul(a64, b64, out=c64)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    tf = 2.0 * m ** 3 / (best / 1e3) / 1e12
+    res["fp64_dgemm_peak"] = {"tflops": tf, "how": "torch.matmul f64 8192^3 (cuBLAS DGEMM), best of 3, CUDA events"}
+    for d in (64, 256, 512):
+        row = res["c5a_mvn_d%d_2p20" % d]
+        row["dense_frac_of_dgemm"] = row["gflops_dense"] / 1e3 / tf
+    del a64, b64, c64
     return res
 
 

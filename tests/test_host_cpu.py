@@ -251,3 +251,30 @@ def test_dist_info_host_only():
     assert i.variable == 1 and i.min_seg_len >= 288 and list(i.tally_seen) == [1, 0, 1]
     with pytest.raises(ValueError):
         shard.dist_info(_lib.DIST_IDS["gamma"], [-1.0, 1.0], [])
+
+
+def test_range_abi_validates_before_touching_a_device():
+    """rs_range_count checks its inputs before any CUDA call (reference rule: validation
+    first, src/continuous.py:413-431), so these run without a GPU."""
+    import ctypes
+
+    from paper_2605_05099_b200 import shard
+
+    r = state_io.create("x256**", seed=[1])
+    fp = shard._fp([0.0, 1.0])
+    ip = shard._ip([])
+    info = _lib.RsRangeInfo()
+
+    def call(rng, dist, entry, L, T):
+        return _lib.lib.rs_range_count(ctypes.byref(rng.to_stream()), _lib.DIST_IDS[dist], fp, ip, entry, L, T,
+                                       ctypes.byref(info), None)
+
+    assert call(r, "norm", 0, 100, 256) == _lib.RS_ERR_VALUE      # seg_len not a multiple of 72
+    assert call(r, "norm", 0, 144, 100) == _lib.RS_ERR_VALUE      # n_seg not a multiple of 256
+    assert call(r, "norm", 144, 144, 256) == _lib.RS_ERR_VALUE    # entry beyond the first segment
+    assert call(r, "u01", 0, 144, 256) == _lib.RS_ERR_UNSUPPORTED  # fixed consumption shards by offsets
+    r.next_u64()                                                   # buffered words: not a fresh position
+    assert call(r, "norm", 0, 144, 256) == _lib.RS_ERR_VALUE
+    assert "fresh" in _lib.last_error()
+    s = state_io.create("sfc64", seed=[1])                          # no skip-ahead
+    assert call(s, "norm", 0, 144, 256) == _lib.RS_ERR_UNSUPPORTED
