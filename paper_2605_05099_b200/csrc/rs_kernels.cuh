@@ -1554,15 +1554,30 @@ __device__ __forceinline__ void stream_rows_lemire(u64 *out, u64 j, u64 nper, bo
     u64 k = 0, stored = 0;  // samples produced / stored (stored: whole chunks)
     const u64 nch = nper / FX_CH;
     const u64 row = (u64)(uintptr_t)(out + j * nper);
-    for (u32 it = 1;; it++) {
-        if (valid && k < nper) {
-            u64 o;
-            if (d.accept(e.next(), o)) {
-                ring[k & 63] = o;
-                k++;
+    for (;;) {
+        // 32 words per flush check, unrolled so the next words' engine steps overlap the
+        // current word's 64x64 product and compare (one stream per thread: ILP is the only
+        // latency hiding at 2^16 streams, ~3.5 warps per SMSP)
+        if (valid && k + 32 <= nper) {
+#pragma unroll 8
+            for (int i = 0; i < 32; i++) {
+                u64 o;
+                const bool ok = d.accept(e.next(), o);
+                ring[k & 63] = o;  // a rejected word's slot is overwritten by the next sample
+                k += ok;
+            }
+        } else {
+            for (int i = 0; i < 32; i++) {
+                if (valid && k < nper) {
+                    u64 o;
+                    if (d.accept(e.next(), o)) {
+                        ring[k & 63] = o;
+                        k++;
+                    }
+                }
             }
         }
-        if ((it & 31) == 0) {
+        {
             const bool ready = valid && k - stored >= FX_CH && stored < nch * FX_CH;
             const u64 dst = ready ? row + stored * 8 : 0;
             const u32 base = (u32)(stored & 63);
