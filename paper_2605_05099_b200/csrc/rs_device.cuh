@@ -1104,8 +1104,15 @@ struct DistLemire {  // bounded_uint(rng, b, 64) discrete.py:20-39 (+ m: bounded
             if (w * b >= thr) return m + __umul64hi(w, b);
         }
     }
-    // word-level form: every lane consumes one word per step (no divergent redraw loops)
+    // word-level form: every lane consumes one word per step (no divergent redraw loops).
+    // For b < 2^32 the 128-bit product w*b needs two 32x32 products, not four.
     RS_DEV bool accept(u64 w, u64 &o) const {
+        if ((b >> 32) == 0) {
+            const u64 lo = (u64)(u32)w * b;                 // w_lo * b
+            const u64 mid = (w >> 32) * b + (lo >> 32);       // w_hi * b + carry, < 2^64
+            o = m + (mid >> 32);                              // high word of w*b
+            return ((mid << 32) | (lo & 0xFFFFFFFFULL)) >= thr;  // low word of w*b
+        }
         o = m + __umul64hi(w, b);
         return w * b >= thr;
     }
