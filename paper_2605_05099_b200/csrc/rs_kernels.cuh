@@ -372,10 +372,13 @@ __device__ __forceinline__ void stage_tables(const FillPlan &p, ZigFast *sm) {
 // then follow by chained products with ML[0] = T^L. Every product is warp-cooperative:
 // lane l owns columns 8l..8l+7 (one coalesced 256-byte read), then a 5-step xor
 // butterfly leaves the result in every lane.
-__device__ __forceinline__ void warp_matvec(const u64 *M, const u64 v[4], u64 out[4]) {
-    int lane = threadIdx.x & 31;
+// One warp-cooperative product with the state held as one byte per lane (lane l: bits
+// 8l..8l+7). Lane l owns columns 8l..8l+7 (one coalesced 256-byte read); the partial sums
+// are then reduce-scattered in 5 halving steps (9 32-bit shuffles) so that every lane ends
+// with exactly its own byte of the product -- the input of the next product.
+__device__ __forceinline__ u32 warp_matvec_rs(const u64 *M, u32 byte) {
+    const u32 lane = threadIdx.x & 31;
     u64 a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-    u32 byte = (u32)((v[lane >> 3] >> (8 * (lane & 7))) & 0xFF);
     const ulonglong2 *c = (const ulonglong2 *)(M + (u64)(8 * lane) * 4);
 #pragma unroll
     for (int k = 0; k < 8; k++) {
@@ -386,36 +389,49 @@ __device__ __forceinline__ void warp_matvec(const u64 *M, const u64 v[4], u64 ou
         a2 ^= y.x & m;
         a3 ^= y.y & m;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        a0 ^= __shfl_xor_sync(0xFFFFFFFFu, a0, o);
-        a1 ^= __shfl_xor_sync(0xFFFFFFFFu, a1, o);
-        a2 ^= __shfl_xor_sync(0xFFFFFFFFu, a2, o);
-        a3 ^= __shfl_xor_sync(0xFFFFFFFFu, a3, o);
-    }
-    out[0] = a0; out[1] = a1; out[2] = a2; out[3] = a3;
+    // lane bit 4 picks the 128-bit half (words 0-1 / 2-3), bit 3 the word, bit 2 the 32-bit
+    // half, bit 1 the 16-bit quarter, bit 0 the byte
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2, b0 = lane & 1;
+    u64 k0 = b4 ? a2 : a0, k1 = b4 ? a3 : a1;
+    k0 ^= __shfl_xor_sync(0xFFFFFFFFu, b4 ? a0 : a2, 16);
+    k1 ^= __shfl_xor_sync(0xFFFFFFFFu, b4 ? a1 : a3, 16);
+    u64 kw = b3 ? k1 : k0;
+    kw ^= __shfl_xor_sync(0xFFFFFFFFu, b3 ? k0 : k1, 8);
+    const u32 lo = (u32)kw, hi = (u32)(kw >> 32);
+    u32 k32 = b2 ? hi : lo;
+    k32 ^= __shfl_xor_sync(0xFFFFFFFFu, b2 ? lo : hi, 4);
+    u32 k16 = b1 ? (k32 >> 16) : (k32 & 0xFFFFu);
+    k16 ^= __shfl_xor_sync(0xFFFFFFFFu, b1 ? (k32 & 0xFFFFu) : (k32 >> 16), 2);
+    u32 k8 = b0 ? (k16 >> 8) : (k16 & 0xFFu);
+    k8 ^= __shfl_xor_sync(0xFFFFFFFFu, b0 ? (k16 & 0xFFu) : (k16 >> 8), 1);
+    return k8;
 }
 
 #ifdef RS_KERNELS_MISC
 __global__ void __launch_bounds__(BLOCK) k_x256_setup(const __grid_constant__ FillPlan p, const u64 *ML,
                                                       u64 *states) {
-    const u32 lane = threadIdx.x & 31;
+    // each lane's byte of its warp's states at steps 0..31 (lane j then reads row j)
+    __shared__ __align__(16) unsigned char sb[BLOCK / 32][32][32];
+    const u32 lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
     const u64 w = ((u64)blockIdx.x * BLOCK + threadIdx.x) >> 5;
     // gridDim.y == 8: interleaved engine, one grid row per lane (base = that lane's state)
     const u64 *b0 = gridDim.y > 1 ? p.lanes + 4 * blockIdx.y : p.base;
     states += (u64)blockIdx.y * 4 * ((u64)gridDim.x * BLOCK);
-    u64 v[4] = {b0[0], b0[1], b0[2], b0[3]};
+    const u64 vq = __ldg(b0 + (lane >> 3));
+    u32 byte = (u32)((vq >> (8 * (lane & 7))) & 0xFF);
     u64 ww = w;
     for (int k = 0; ww; k++, ww >>= 1)
-        if (ww & 1) warp_matvec(ML + (u64)(1 + k) * 1024, v, v);
-    u64 mine[4] = {v[0], v[1], v[2], v[3]};
+        if (ww & 1) byte = warp_matvec_rs(ML + (u64)(1 + k) * 1024, byte);
+    sb[wi][0][lane] = (unsigned char)byte;
     for (u32 j = 1; j < 32; j++) {
-        warp_matvec(ML, v, v);
-        if (lane == j) { mine[0] = v[0]; mine[1] = v[1]; mine[2] = v[2]; mine[3] = v[3]; }
+        byte = warp_matvec_rs(ML, byte);
+        sb[wi][j][lane] = (unsigned char)byte;
     }
+    __syncwarp();
+    const ulonglong2 *row = (const ulonglong2 *)&sb[wi][lane][0];
     ulonglong2 *d = (ulonglong2 *)(states + 4 * (32 * w + lane));
-    d[0] = make_ulonglong2(mine[0], mine[1]);
-    d[1] = make_ulonglong2(mine[2], mine[3]);
+    d[0] = row[0];
+    d[1] = row[1];
 }
 #endif  // RS_KERNELS_MISC
 
