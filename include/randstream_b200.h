@@ -162,6 +162,14 @@ rs_status rs_fill_streams(int32_t engine, const uint64_t *seed, int32_t n_seed,
 rs_status rs_mvn(rs_stream *stream, const double *L, const double *mean, int64_t d, uint64_t n,
                  int32_t layout, double *out, rs_fill_result *result, void *cuda_stream);
 
+/* The contraction half of rs_mvn, for a caller that drew z itself (rs_fill of
+ * RS_DIST_STDNORM, n*d values, device memory): x = mean + z @ L^T. It lets the
+ * host factorise the covariance while the z fill runs (the reference computes
+ * L first, continuous.py:312-336; the Python layer restores the stream if the
+ * factorisation fails, so the observable order is the same). */
+rs_status rs_mvn_apply(const double *L, const double *mean, int64_t d, uint64_t n, int32_t layout,
+                       const double *z_device, double *out, void *cuda_stream);
+
 /* ---- multi-GPU sharding of variable-consumption fills ----
  * Replaces nothing one-for-one in the reference: it is the rank-local half of
  * `Rng.fill(dist, params, n)` (rng.py:223-241) when one logical stream is split

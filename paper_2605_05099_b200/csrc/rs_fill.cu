@@ -1116,15 +1116,17 @@ rs_status rs_fill_streams(int32_t engine, const uint64_t *seed, int32_t n_seed, 
     return RS_OK;
 }
 
-rs_status rs_mvn(rs_stream *s, const double *L, const double *mean, int64_t d, uint64_t n, int32_t layout,
-                 double *out, rs_fill_result *result, void *cuda_stream) {
+// rs_mvn (zext == nullptr: z drawn here from `s`) and rs_mvn_apply (z given, on the device)
+static rs_status mvn_core(rs_stream *s, const double *L, const double *mean, int64_t d, uint64_t n, int32_t layout,
+                          const double *zext, double *out, rs_fill_result *result, void *cuda_stream) {
     if (d < 1 || n < 1) { rs::set_error("mvn needs n >= 1"); return RS_ERR_VALUE; }
     if (layout != 0 && layout != 1) { rs::set_error("mvn layout must be 'n_d' or 'd_n'"); return RS_ERR_VALUE; }
     rs_status rc;
     int dev;
     {
         std::lock_guard<std::mutex> g(g_mu);
-        if ((rc = check_stream(s))) return rc;
+        if (!zext && (rc = check_stream(s))) return rc;
+        if (zext && !is_device_ptr(zext)) { rs::set_error("mvn z must be device memory"); return RS_ERR_VALUE; }
         if (is_device_ptr(out)) {
             cudaPointerAttributes a;
             CK(cudaPointerGetAttributes(&a, out));
@@ -1142,7 +1144,7 @@ rs_status rs_mvn(rs_stream *s, const double *L, const double *mean, int64_t d, u
     cudaStream_t st = (cudaStream_t)cuda_stream;
     size_t nz = (size_t)n * (size_t)d;
     // z and the factor / mean in device memory
-    size_t need = nz * 8 + (size_t)d * d * 8 + (size_t)d * 8;
+    size_t need = (zext ? 0 : nz * 8) + (size_t)d * d * 8 + (size_t)d * 8;
     {
         std::lock_guard<std::mutex> g(g_mu);
         if (need > c->mvn_bytes) {
@@ -1155,11 +1157,13 @@ rs_status rs_mvn(rs_stream *s, const double *L, const double *mean, int64_t d, u
             if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) { rs::set_error("cublasCreate failed"); return RS_ERR_CUDA; }
         }
     }
-    double *z = c->mvn_z, *Ld = z + nz, *md = Ld + (size_t)d * d;
+    double *zbuf = c->mvn_z, *Ld = zbuf + (zext ? 0 : nz), *md = Ld + (size_t)d * d;
+    const double *z = zext ? zext : zbuf;
     CK(cudaMemcpyAsync(Ld, L, (size_t)d * d * 8, cudaMemcpyDefault, st));
     CK(cudaMemcpyAsync(md, mean, (size_t)d * 8, cudaMemcpyDefault, st));
     rs_fill_result fr;
-    if ((rc = rs_fill(s, RS_DIST_STDNORM, nullptr, nullptr, nz, z, &fr, cuda_stream))) return rc;
+    memset(&fr, 0, sizeof fr);
+    if (!zext && (rc = rs_fill(s, RS_DIST_STDNORM, nullptr, nullptr, nz, zbuf, &fr, cuda_stream))) return rc;
     std::lock_guard<std::mutex> g(g_mu);
     bool host_out = !is_device_ptr(out);
     double *X;
@@ -1243,6 +1247,16 @@ rs_status rs_mvn(rs_stream *s, const double *L, const double *mean, int64_t d, u
     if (result) *result = fr;
     rs::clear_error();
     return RS_OK;
+}
+
+rs_status rs_mvn(rs_stream *s, const double *L, const double *mean, int64_t d, uint64_t n, int32_t layout,
+                 double *out, rs_fill_result *result, void *cuda_stream) {
+    return mvn_core(s, L, mean, d, n, layout, nullptr, out, result, cuda_stream);
+}
+
+rs_status rs_mvn_apply(const double *L, const double *mean, int64_t d, uint64_t n, int32_t layout,
+                       const double *z_device, double *out, void *cuda_stream) {
+    return mvn_core(nullptr, L, mean, d, n, layout, z_device, out, nullptr, cuda_stream);
 }
 
 // ----------------------------------------------------------------------------- sharded fills

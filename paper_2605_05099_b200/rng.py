@@ -506,18 +506,41 @@ class Rng:
         if n < 1:
             raise ValueError("mvn needs n >= 1")
         d = mean.size
-        factor = np.ascontiguousarray(semidefinite_factor(cov))
         dev = self._device()
         out = torch.empty((n, d) if layout == "n_d" else (d, n), dtype=torch.float64, device=dev)
-        st = self.to_stream()
-        res = _lib.RsFillResult()
+        z = torch.empty(n * d, dtype=torch.float64, device=dev)
+        # The host factorises S while the device draws z (both release the GIL). The
+        # reference factorises first (continuous.py:312-336), so a failed factorisation
+        # puts the generator back where it was: nothing observable is consumed.
+        before = (list(self.engine.s), self.buffer.capture(), {k: dict(v) for k, v in self.counters.items()})
+        fut = _host_pool().submit(semidefinite_factor, cov)
+        try:
+            self.device_fill("stdnorm", [], [], n * d, out=z)
+        finally:
+            try:
+                factor = np.ascontiguousarray(fut.result())
+            except Exception:
+                self.engine.s, self.counters = before[0], before[2]
+                self.buffer.restore(before[1])
+                raise
         mptr = np.ascontiguousarray(mean)
-        _lib.check(_lib.lib.rs_mvn(ctypes.byref(st), ctypes.c_void_p(factor.ctypes.data),
-                                   mptr.ctypes.data_as(_lib.DBLP), d, n, 0 if layout == "n_d" else 1,
-                                   ctypes.c_void_p(out.data_ptr()), ctypes.byref(res), _cuda_stream_ptr(dev)))
-        self.from_stream(st)
-        self._add_tallies(res)
+        _lib.check(_lib.lib.rs_mvn_apply(ctypes.c_void_p(factor.ctypes.data), mptr.ctypes.data_as(_lib.DBLP), d, n,
+                                         0 if layout == "n_d" else 1, ctypes.c_void_p(z.data_ptr()),
+                                         ctypes.c_void_p(out.data_ptr()), _cuda_stream_ptr(dev)))
         return out
+
+
+_POOL = None
+
+
+def _host_pool():
+    """One worker thread for host work that overlaps a device fill (mvn's factorisation)."""
+    global _POOL
+    if _POOL is None:
+        import concurrent.futures
+
+        _POOL = concurrent.futures.ThreadPoolExecutor(1, thread_name_prefix="randstream-host")
+    return _POOL
 
 
 def semidefinite_factor(cov):

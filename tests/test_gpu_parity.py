@@ -584,3 +584,22 @@ def test_gamma_family_with_and_without_speculative_store(monkeypatch, dist, para
         assert np.array_equal(_bits(got), _bits(ref)), flag
         _assert_same_position(r, o, str(flag))
         assert r.counters == o.tallies()
+
+
+def test_mvn_indefinite_covariance_consumes_nothing():
+    """The factorisation overlaps the z fill, but a covariance that is not positive
+    semidefinite still fails with the stream untouched (the reference factorises first,
+    continuous.py:293-336)."""
+    r = state_io.create("philox", seed=[31])
+    r.next_u64()  # mid-buffer
+    before = _state_of(r)
+    S = np.array([[1.0, 2.0], [2.0, 1.0]])  # eigenvalues 3 and -1
+    with pytest.raises(ValueError, match="positive semidefinite"):
+        r.mvn(np.zeros(2), S, n=1000)
+    assert _state_of(r) == before and r.counters == {}
+    # and then the stream continues exactly as the oracle's
+    o = O.OracleRng("philox", seed=[31])
+    o.next_u64()
+    ref = o.fill("norm", {}, 5000)
+    got = r.fill("norm", {}, 5000).cpu().numpy()
+    assert np.array_equal(_bits(got), _bits(ref))
