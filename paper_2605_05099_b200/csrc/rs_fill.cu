@@ -677,7 +677,10 @@ rs_status prep_chunk(DevCtx &c, FillPlan &p, const Resolved &r, bool mem, cudaSt
         p.bm = c.bm;
     }
     p.spec = nullptr;
-    if (r.family == FAM_GAMMA && r.kind != GK_T && !getenv("RS_NO_SPEC")) {
+    // the store costs ~36 bytes per provisioned sample slot; past 16 GiB (a 2^29-sample
+    // gamma fill) the three-parse path keeps the scratch bounded
+    const size_t spec_est = (size_t)p.T * (p.L / (r.kind != GK_GAMMA ? 4 : 2) + 8) * 36;
+    if (r.family == FAM_GAMMA && r.kind != GK_T && !getenv("RS_NO_SPEC") && spec_est <= (16ULL << 30)) {
         // an attempt draws 2 words, so a segment of L words starts <= L/2 + 1 samples
         // (<= L/4 + 1 for the paired laws: two gamma sub-samples per sample)
         const bool paired = r.kind != GK_GAMMA;
