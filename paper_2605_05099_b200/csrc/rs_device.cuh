@@ -1263,9 +1263,9 @@ struct RingWriter {
 // complete group. A lane's groups then leave on the same steps as its neighbours'
 // instead of a divergent flush on nearly every step (some lane of 32 is always at its
 // group end). Buffered samples stay below 2G: <= G-1 after a tick, + G before the next.
-template <class T, int NT>
+template <class T, int NT, int GB = 32>  // GB: bytes per group (32: one STG.256)
 struct BatchRing {
-    static constexpr int G = 32 / (int)sizeof(T);
+    static constexpr int G = GB / (int)sizeof(T);
     T *abase;  // 32-byte aligned base
     u64 pos;   // element index (from abase) of the next sample
     u64 fl;    // first element not yet stored
@@ -1286,18 +1286,23 @@ struct BatchRing {
         T *p = abase + g0;
         int b = (int)(g0 & (2 * G - 1));  // ring slot of the group's first element
         if (fl == g0) {
-            u64 q[4];
+            constexpr int E32 = 32 / (int)sizeof(T);  // elements per 32-byte store
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-                if constexpr (sizeof(T) == 8) {
-                    q[k] = *(const u64 *)&ring[(b + k) * NT];
-                } else {
-                    u64 lo = *(const u32 *)&ring[(b + 2 * k) * NT], hi = *(const u32 *)&ring[(b + 2 * k + 1) * NT];
-                    q[k] = lo | (hi << 32);
+            for (int h = 0; h < GB / 32; h++) {
+                u64 q[4];
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    if constexpr (sizeof(T) == 8) {
+                        q[k] = *(const u64 *)&ring[(b + h * E32 + k) * NT];
+                    } else {
+                        u64 lo = *(const u32 *)&ring[(b + h * E32 + 2 * k) * NT];
+                        u64 hi = *(const u32 *)&ring[(b + h * E32 + 2 * k + 1) * NT];
+                        q[k] = lo | (hi << 32);
+                    }
                 }
+                asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p + h * E32), "l"(q[0]), "l"(q[1]),
+                             "l"(q[2]), "l"(q[3]) : "memory");
             }
-            asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(q[0]), "l"(q[1]), "l"(q[2]),
-                         "l"(q[3]) : "memory");
         } else {  // the run's first group is shared with the previous run
             for (int k = (int)(fl - g0); k < G; k++) p[k] = ring[(b + k) * NT];
         }

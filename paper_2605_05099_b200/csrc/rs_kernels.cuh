@@ -435,6 +435,9 @@ __global__ void __launch_bounds__(BLOCK) k_x256_setup(const __grid_constant__ Fi
 }
 #endif  // RS_KERNELS_MISC
 
+// bytes per BatchRing group in k_emit (one group leaves per tick as GB/32 STG.256)
+constexpr int EMIT_GB = 64;
+
 // resident blocks per SM the parse kernels are compiled for (register budget)
 constexpr int minb(int E, int D) {
     return D == FAM_GAMMA ? 2 : (D == FAM_LEMIRE || D == FAM_U32) ? 4 : 3;
@@ -909,7 +912,7 @@ template <int E, int D>
 __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constant__ FillPlan p, const u32 *entry, const u64 *cnt,
                                                 const u64 *off, const u32 *ex, DevResult *res) {
     __shared__ ZigFast sm[256];
-    __shared__ __align__(16) unsigned char ring_sm[64 * BLOCK];  // RingWriter: 32 B, BatchRing: 64 B per thread
+    __shared__ __align__(16) unsigned char ring_sm[2 * EMIT_GB * BLOCK];  // RingWriter: 32 B, BatchRing: 2 groups per thread
     stage_tables(p, sm);
     u32 t = blockIdx.x * BLOCK + threadIdx.x;
     Tally tl = {0, 0, 0, 0, 0};
@@ -1026,7 +1029,7 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constan
             typedef typename DistOf<D>::type::out_t T;
             T *ring = (T *)ring_sm + threadIdx.x;
             if constexpr (D == FAM_LEMIRE || D == FAM_U32) {  // one unit per step, <= 1 sample
-                BatchRing<T, BLOCK> wr;
+                BatchRing<T, BLOCK, EMIT_GB> wr;
                 wr.init((T *)p.out, p.out0 + o, ring);
                 u32 it = 0;
                 for (u64 k = 0; k < kmax;) {
@@ -1035,14 +1038,14 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constan
                     if constexpr (D == FAM_LEMIRE) ok = d.accept(s.next(), v);
                     else ok = d.accept(s.next32(), v);
                     if (ok) { wr.put(v); k++; }
-                    if ((++it & (BatchRing<T, BLOCK>::G - 1)) == 0) wr.tick();
+                    if ((++it & (BatchRing<T, BLOCK, EMIT_GB>::G - 1)) == 0) wr.tick();
                 }
                 wr.finish();
             } else {
                 bool done = false;
                 if constexpr (D == FAM_NORM || D == FAM_EXP) {
                     if (d.word_level()) {
-                        BatchRing<T, BLOCK> wr;
+                        BatchRing<T, BLOCK, EMIT_GB> wr;
                         wr.init((T *)p.out, p.out0 + o, ring);
                         wl_emit(d, s, kmax, wr, tl);
                         wr.finish();
@@ -1051,14 +1054,14 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constan
                 }
                 if constexpr (D == FAM_GAMMA) {
                     if (d.am_applies()) {  // one attempt per step, <= 1 sample
-                        BatchRing<T, BLOCK> wr;
+                        BatchRing<T, BLOCK, EMIT_GB> wr;
                         wr.init((T *)p.out, p.out0 + o, ring);
                         GammaAM m{0, 0, 0.0};
                         u32 it = 0;
                         for (u64 k = 0; k < kmax;) {
                             double v;
                             if (d.am_step(m, s, tl, v)) { wr.put(v); k++; }
-                            if ((++it & (BatchRing<T, BLOCK>::G - 1)) == 0) wr.tick();
+                            if ((++it & (BatchRing<T, BLOCK, EMIT_GB>::G - 1)) == 0) wr.tick();
                         }
                         wr.finish();
                         done = true;
