@@ -199,6 +199,41 @@ RS_DEV void philox4x64_10_rk(u64 c0, u64 c1, u64 c2, u64 c3, const u64 *rk0, con
     o0 = c0; o1 = c1; o2 = c2; o3 = c3;
 }
 
+// The same bijection when counter words 1-3 are launch constants (no carry out of
+// word 0 anywhere in the launch). Round 0's c2 product and round 1's c0 product then
+// depend only on words 1-3 and the keys, so they are folded into four per-thread
+// constants (philox_fold) and each block costs 18 products instead of 20.
+struct PhiloxFold { u64 ka, kb, kc, kd; };
+RS_DEV PhiloxFold philox_fold(u64 c1, u64 c2, u64 c3, const u64 *rk0, const u64 *rk1) {
+    u64 lo1, hi1, lo0, hi0;
+    mul64x64(0xCA5A826395121157ULL, c2, lo1, hi1);        // round 0, c2 product
+    u64 n0 = hi1 ^ c1 ^ rk0[0];                            // round-1 c0
+    mul64x64(0xD2E7470EE14C6C93ULL, n0, lo0, hi0);         // round 1, c0 product
+    return PhiloxFold{c3 ^ rk1[0], lo1 ^ rk0[1], hi0 ^ rk1[1], lo0};
+}
+template <int V = 0>
+RS_DEV void philox4x64_10_folded(u64 c0, const PhiloxFold &f, const u64 *rk0, const u64 *rk1, u64 &o0, u64 &o1,
+                                 u64 &o2, u64 &o3) {
+    u64 lo0, hi0, lo1, hi1;
+    mul64x64(0xD2E7470EE14C6C93ULL, c0, lo0, hi0);         // round 0, c0 product
+    mul64x64(0xCA5A826395121157ULL, hi0 ^ f.ka, lo1, hi1);  // round 1, c2 product
+    u64 c1 = lo1, c2 = lo0 ^ f.kc, c3 = f.kd;
+    c0 = hi1 ^ f.kb;
+#pragma unroll
+    for (int r = 2; r < 10; r++) {
+        if constexpr (V == 0) {
+            mul64x64(0xD2E7470EE14C6C93ULL, c0, lo0, hi0);
+            mul64x64(0xCA5A826395121157ULL, c2, lo1, hi1);
+        } else {
+            mul64x64_cc(0xD2E7470EE14C6C93ULL, c0, lo0, hi0);
+            mul64x64_cc(0xCA5A826395121157ULL, c2, lo1, hi1);
+        }
+        u64 n0 = hi1 ^ c1 ^ rk0[r], n2 = hi0 ^ c3 ^ rk1[r];
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    }
+    o0 = c0; o1 = c1; o2 = c2; o3 = c3;
+}
+
 struct EngPhilox {  // counter.py:98-121; words of a block are served x0..x3
     u64 c0, c1, c2, c3, k0, k1;
     u64 b0, b1, b2, b3;

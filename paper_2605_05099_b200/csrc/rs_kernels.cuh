@@ -1234,6 +1234,9 @@ __global__ void __launch_bounds__(BLOCK) k_fixed(const __grid_constant__ FillPla
 // Counter-based fixed fills (Philox-4x64-10, counter.py:98-121): word w of the
 // stream is block(ctr0 + w/4)[w % 4], so threads take lane-consecutive blocks in
 // a grid-stride loop and each warp store is one contiguous 1 KB (STG.256 per lane).
+template <int MODE, int V, bool FOLD>
+__device__ __forceinline__ void philox_fixed_loop(const FillPlan &p, const PhiloxFold &f, u64 b, u64 nblk,
+                                                  u64 stride);
 template <int MODE, int V = 0>
 __global__ void __launch_bounds__(BLOCK) k_philox_fixed(const __grid_constant__ FillPlan p) {
     const u64 nblk = (p.weng + 3) / 4;
@@ -1254,15 +1257,33 @@ __global__ void __launch_bounds__(BLOCK) k_philox_fixed(const __grid_constant__ 
             for (int i = 0; i < p.P && (u64)i < p.n; i++) out[i] = fx_map<MODE>(p, p.prefix[i]);
         }
     }
+    // No carry out of counter word 0 over the launch's blocks (launch-uniform): words
+    // 1-3 are constants and the first two rounds fold (philox4x64_10_folded). Blocks
+    // at bb >= nblk are computed but never stored, so they need not satisfy it.
+    if (nblk > 0 && p.base[0] + (nblk - 1) >= p.base[0]) {
+        const PhiloxFold f = philox_fold(p.base[1], p.base[2], p.base[3], p.rk0, p.rk1);
+        philox_fixed_loop<MODE, V, true>(p, f, b, nblk, stride);
+    } else {
+        philox_fixed_loop<MODE, V, false>(p, PhiloxFold{}, b, nblk, stride);
+    }
+}
+
+template <int MODE, int V, bool FOLD>
+__device__ __forceinline__ void philox_fixed_loop(const FillPlan &p, const PhiloxFold &f, u64 b, u64 nblk,
+                                                  u64 stride) {
     // two independent blocks per iteration (ILP for the IMAD pipe)
     for (; b < nblk; b += 2 * stride) {
         u64 w[2][4];
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             u64 bb = b + h * stride;
-            u64 c0 = p.base[0] + bb, c1 = p.base[1], c2 = p.base[2], c3 = p.base[3];
-            if (c0 < bb) { if (++c1 == 0) { if (++c2 == 0) ++c3; } }
-            philox4x64_10_rk<V>(c0, c1, c2, c3, p.rk0, p.rk1, w[h][0], w[h][1], w[h][2], w[h][3]);
+            if constexpr (FOLD) {
+                philox4x64_10_folded<V>(p.base[0] + bb, f, p.rk0, p.rk1, w[h][0], w[h][1], w[h][2], w[h][3]);
+            } else {
+                u64 c0 = p.base[0] + bb, c1 = p.base[1], c2 = p.base[2], c3 = p.base[3];
+                if (c0 < bb) { if (++c1 == 0) { if (++c2 == 0) ++c3; } }
+                philox4x64_10_rk<V>(c0, c1, c2, c3, p.rk0, p.rk1, w[h][0], w[h][1], w[h][2], w[h][3]);
+            }
         }
 #pragma unroll
         for (int h = 0; h < 2; h++) {

@@ -381,6 +381,26 @@ def test_c1_full_2p30_windows():
     del t
 
 
+@pytest.mark.parametrize("ctr", [
+    [2 ** 64 - 1000, 2 ** 64 - 1, 5, 0],            # carry out of word 0 (and 1) inside the fill
+    [2 ** 63 + 12345, 0xDEADBEEF, 2 ** 64 - 1, 77],  # no carry: words 1-3 fold into launch constants
+])
+@pytest.mark.parametrize("dist", ["u01", "u01f", "uint64"])
+def test_philox_counter_words(ctr, dist):
+    """k_philox_fixed folds rounds 0-1 when counter words 1-3 are launch constants and
+    takes the general path when word 0 carries (counter.py:98-121)."""
+    r = state_io.create("philox", seed=[3])
+    o = O.OracleRng("philox", seed=[3])
+    st = ctr + o.get_state()[4:]
+    r.set_state(st)
+    o.set_state(st)
+    params = {}
+    n = (1 << 16) + 5
+    got = _np(r.fill(dist, params, n))
+    assert np.array_equal(_bits(got), _bits(o.fill(dist, params, n)))
+    _assert_same_position(r, o)
+
+
 @pytest.mark.slow
 def test_c2_full_2p30_windows():
     n = 1 << 30
