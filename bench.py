@@ -260,7 +260,8 @@ def run_ours(args, rank, world, local_rank):
         traffic = pj.get("traffic_bytes_per_launch")
         heavy = pj["metrics"].get("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed", {}).get("value")
         if heavy:
-            limiter = ("integer multiply: Philox-4x64-10 needs 80 IMAD.WIDE.U32 per 4-word block; ncu: fmaheavy "
+            limiter = ("integer multiply: Philox-4x64-10 needs 72 IMAD.WIDE.U32 per 4-word block (18 products after the "
+                       "round fold, DESIGN 4.1); ncu: fmaheavy "
                        "pipe %.1f%% busy, DRAM %.1f%% (profiles/r01_ncu_philox_u01_f64.json)" % (
                            heavy, pj["metrics"]["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]["value"]))
     line = {
