@@ -1234,6 +1234,9 @@ __global__ void __launch_bounds__(BLOCK) k_fixed(const __grid_constant__ FillPla
 // Counter-based fixed fills (Philox-4x64-10, counter.py:98-121): word w of the
 // stream is block(ctr0 + w/4)[w % 4], so threads take lane-consecutive blocks in
 // a grid-stride loop and each warp store is one contiguous 1 KB (STG.256 per lane).
+#ifndef RS_PHILOX_ILP
+#define RS_PHILOX_ILP 1  // blocks per thread and iteration: 1 (32 registers) beat 2/3/4 on B200, DESIGN 4.1
+#endif
 template <int MODE, int V, bool FOLD>
 __device__ __forceinline__ void philox_fixed_loop(const FillPlan &p, const PhiloxFold &f, u64 b, u64 nblk,
                                                   u64 stride);
@@ -1271,11 +1274,11 @@ __global__ void __launch_bounds__(BLOCK) k_philox_fixed(const __grid_constant__ 
 template <int MODE, int V, bool FOLD>
 __device__ __forceinline__ void philox_fixed_loop(const FillPlan &p, const PhiloxFold &f, u64 b, u64 nblk,
                                                   u64 stride) {
-    // two independent blocks per iteration (ILP for the IMAD pipe)
-    for (; b < nblk; b += 2 * stride) {
-        u64 w[2][4];
+    // RS_PHILOX_ILP blocks per iteration (higher ILP measured slower: more registers, fewer warps)
+    for (; b < nblk; b += RS_PHILOX_ILP * stride) {
+        u64 w[RS_PHILOX_ILP][4];
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
+        for (int h = 0; h < RS_PHILOX_ILP; h++) {
             u64 bb = b + h * stride;
             if constexpr (FOLD) {
                 philox4x64_10_folded<V>(p.base[0] + bb, f, p.rk0, p.rk1, w[h][0], w[h][1], w[h][2], w[h][3]);
@@ -1286,7 +1289,7 @@ __device__ __forceinline__ void philox_fixed_loop(const FillPlan &p, const Philo
             }
         }
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
+        for (int h = 0; h < RS_PHILOX_ILP; h++) {
             u64 bb = b + h * stride;
             if (bb >= nblk) break;
             u64 q0 = fx_map<MODE>(p, w[h][0]), q1 = fx_map<MODE>(p, w[h][1]);
