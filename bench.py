@@ -12,16 +12,20 @@ fixed ("weak") and there is no collective on the data path.
             events on the launch stream, max over ranks)
   e2e       the same fills through the public API with pinned HOST output
             buffers (library stages through HBM; D2H inside the timed region)
-  roofline  the dominant kernel (u01 f64 fill): algorithmic bytes 8 B/sample x
-            2^30 per launch / its average CUDA-event duration, against the
-            measured HBM figure in MEASURED_PEAKS.json
+  roofline  the dominant kernel (k_philox_fixed, u01 f64): it is bound by the
+            integer-multiply (fmaheavy) pipe, not HBM -- `frac` is its 64x64->128
+            products per second against that pipe's capacity; the HBM fraction of
+            the same launch is reported beside it
   cpu_baseline  the C restatement of the reference (oracle/, "port") on all
             host threads, each on a disjoint counter-offset substream
-  per_config    device-time Gsamples/s of the other BASELINE configs (N=1 only)
+  per_config    every other BASELINE row (N=1 only), each timed through the product
+            call (Rng.fill / fill_streams / Rng.mvn, CUDA events on the stream),
+            with its roofline fraction and the same-run CPU rate of the port at
+            P = all host threads and P = 1 (same partition scheme as the GPU)
 
---impl reference runs the reference's CPU path (the oracle port; the Python
-reference itself is not on the GPU box) on the same metric and prints
-"impl": "reference".
+--impl reference runs the reference's CPU path (the oracle port: the reference is
+pure Python and is not on the GPU box) on the headline's full config -- 2^30 u01 +
+2^30 u01f per GPU per step, all host threads -- and prints "impl": "reference".
 """
 
 import argparse
@@ -52,7 +56,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-per-config", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=3.0)
+    ap.add_argument("--cpu-seconds", type=float, default=1.0)
+    ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 
 
@@ -66,38 +71,98 @@ def measured_peaks():
 
 
 # ------------------------------------------------------------------ CPU reference / baseline
-def cpu_reference(seconds, dist_pairs=(("u01", 8), ("u01f", 4))):
-    """Oracle port on all host threads: thread t fills from the counter-offset slice t of
-    the philox seed-7 stream (full mantissa), repeated 2^22-sample fills (bench.py of the
-    reference fills fixed-size buffers the same way, src/bench.py:50-67)."""
-    from oracle import oracle as O
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-    P = O.cpu_count()
-    m = 1 << 22
-    rngs = {}
-    for dist, _ in dist_pairs:
-        rs = []
-        for t in range(P):
+
+class C2Reference:
+    """The headline config on the host: the oracle port (C restatement of the reference),
+    P threads, thread t filling counter-offset slice t of the philox seed-7 stream (full
+    mantissa) -- the GPU's partition (counter.py:108-112). One step = u01 f64 2^30 plus
+    u01f f32 2^30 per GPU of the run, into preallocated host arrays."""
+
+    def __init__(self, world=1):
+        from oracle import oracle as O
+        self.O = O
+        self.P = O.cpu_count()
+        self.world = world
+        self.per = {d: (N_HEAD // self.P + 7) // 8 * 8 for d in ("u01", "u01f")}
+        self.outs = {d: [np.empty(self.per[d], dtype=np.float64 if d == "u01" else np.float32)
+                         for _ in range(self.P)] for d in ("u01", "u01f")}
+
+    def rngs(self, dist, g):
+        O = self.O
+        out = []
+        for t in range(self.P):
             o = O.OracleRng("philox", seed=[7], full_mantissa=True)
             st = o.get_state()
-            words_per_thread = 1 << 34
-            if dist == "u01f":
-                words_per_thread //= 2
-            st[0] = (st[0] + t * (words_per_thread // 4)) & (2 ** 64 - 1)
+            w0 = g * N_HEAD + t * self.per[dist]  # first sample of the slice
+            words = w0 if dist == "u01" else w0 // 2
+            st[0] = (st[0] + words // 4) & (2 ** 64 - 1)
             o.set_state(st)
-            rs.append(o)
-        rngs[dist] = rs
-    done = 0
-    t0 = time.perf_counter()
+            out.append(o)
+        return out
+
+    def step(self):
+        t0 = time.perf_counter()
+        for g in range(self.world):
+            for dist in ("u01", "u01f"):
+                self.O.threaded_fill(self.rngs(dist, g), dist, {}, self.per[dist], self.outs[dist])
+        return time.perf_counter() - t0
+
+    def sample(self):
+        return ("%d host threads (%s): the full config, %d x (2^30 u01 f64 + 2^30 u01f f32) per step, thread t = "
+                "counter-offset slice t" % (self.P, cpu_model(), self.world))
+
+
+def cpu_rate(engine, seed, dist, params, P, seconds, fm=False, spawn_streams=False):
+    """Samples/s of the oracle port on P host threads, each on a disjoint substream of the
+    engine (offset t * 2^50 words) or, for per-stream mode, its own spawned stream."""
+    from oracle import oracle as O
+
+    rngs = []
+    for t in range(P):
+        if spawn_streams:
+            o = O.OracleRng(engine, seed=seed, spawn_key=(t,))
+        else:
+            o = O.OracleRng(engine, seed=seed)
+            st = o.get_state()
+            off = t << 50
+            if engine == "philox":
+                st[0] = (st[0] + off // 4) & (2 ** 64 - 1)
+            elif engine == "x256**":
+                st = O.x256_apply_poly(st, O.x_pow_mod(off, O.x256_charpoly()))
+            elif engine == "pcg64":
+                st = O.pcg_advance(st, off)
+            elif engine == "ranlux++":
+                st = O.ranlux_advance_chunks(st, off // 9)
+            o.set_state(st)
+        o.set_full_mantissa(fm)
+        rngs.append(o)
+    m = 1 << 12
+    outs = None
+    while True:  # size one call at ~50 ms
+        t0 = time.perf_counter()
+        O.threaded_fill(rngs, dist, params, m)
+        if time.perf_counter() - t0 > 0.05 or m >= 1 << 26:
+            break
+        m *= 4
+    outs = [np.empty(m, dtype=O.out_dtype(dist)) for _ in range(P)]
+    done, t0 = 0, time.perf_counter()
     while True:
-        for dist, _ in dist_pairs:
-            O.threaded_fill(rngs[dist], dist, {}, m)
-            done += P * m
+        O.threaded_fill(rngs, dist, params, m, outs)
+        done += P * m
         el = time.perf_counter() - t0
         if el >= seconds:
             break
-    return done / el / 1e9, P, "%d host threads x repeated 2^22-sample philox fills (u01 f64 + u01f f32), %.1f s" % (
-        P, el)
+    return {"gsamples_s": done / el / 1e9, "cores": P, "seconds": round(el, 3), "per_call": m}
 
 
 # ------------------------------------------------------------------ clocks
@@ -247,23 +312,31 @@ def run_ours(args, rank, world, local_rank):
 
     per_config = None
     if world == 1 and not args.no_per_config:
-        per_config = run_per_config(dev, stream, sptr, out64, peak)
+        per_config = run_per_config(dev, stream, sptr, out64, peak, args.cpu_seconds, not args.no_cpu)
     sharded = None
     if world > 1 and not args.no_per_config:
         sharded = run_sharded(rank, world, dev)
 
-    traffic, limiter = None, None
+    # Roofline of the dominant kernel. k_philox_fixed is bound by the integer multiplies,
+    # not by HBM (DESIGN 4.1): Philox-4x64-10 needs 20 64x64->128 products per 4-word
+    # block, 18 after the round fold. A 64x64 product is four IMAD.WIDE.U32, and one
+    # IMAD.WIDE warp instruction holds an SMSP's fmaheavy pipe 4 cycles, so the pipe
+    # completes 2 products per cycle per SMSP: 148 SMs x 4 SMSPs x 2 x f_max.
+    mhz = clocks.get("sm_max_mhz") or 1965.0
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    int_peak = sms * 4 * 2 * mhz * 1e6 / 1e9  # G products/s
+    prods = 18.0 * (N_HEAD / 4)               # products per u01 launch (folded rounds)
+    int_achieved = prods / (avg64 / 1e3) / 1e9
+    traffic, pipe = None, None
     prof = os.path.join(ROOT, "profiles", "r01_ncu_philox_u01_f64.json")
     if os.path.exists(prof):
         with open(prof) as f:
             pj = json.load(f)
         traffic = pj.get("traffic_bytes_per_launch")
-        heavy = pj["metrics"].get("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed", {}).get("value")
-        if heavy:
-            limiter = ("integer multiply: Philox-4x64-10 needs 72 IMAD.WIDE.U32 per 4-word block (18 products after the "
-                       "round fold, DESIGN 4.1); ncu: fmaheavy "
-                       "pipe %.1f%% busy, DRAM %.1f%% (profiles/r01_ncu_philox_u01_f64.json)" % (
-                           heavy, pj["metrics"]["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]["value"]))
+        pipe = {"fmaheavy_busy_pct": pj["metrics"].get(
+                    "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed", {}).get("value"),
+                "dram_busy_pct": pj["metrics"]["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]["value"],
+                "source": "profiles/r01_ncu_philox_u01_f64.json (ncu --set full, same kernel)"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -273,12 +346,17 @@ def run_ours(args, rank, world, local_rank):
                                "+ u01f f32 n=2^30 per GPU; rank g = counter-offset slice g",
                    "l2": "outputs 12 GiB per step >> 126 MB L2 (inputs larger than L2, no flush)",
                    "parallelism": "dp%d (independent counter slices, no collective)" % world},
-        "roofline": {"bound": "hbm", "kernel": "k_philox_fixed<FX_U01> (u01 f64 fill)", "achieved": achieved,
-                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                     "traffic_unit": "DRAM bytes per launch (ncu --set full, same kernel)", "limiter": limiter,
-                     "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes64,
-                     "avg_launch_ms": avg64, "u01f_f32_launch_ms": avg32,
-                     "u01f_f32_achieved_gbs": 4.0 * N_HEAD / (avg32 / 1e3) / 1e9},
+        "roofline": {"bound": "int", "pipe": "fmaheavy (IMAD.WIDE, integer multiply)",
+                     "kernel": "k_philox_fixed<FX_U01> (u01 f64 fill)",
+                     "achieved": int_achieved, "peak": int_peak, "unit": "G 64x64->128-bit products/s",
+                     "frac": int_achieved / int_peak, "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per launch (ncu --set full, same kernel)",
+                     "peak_source": "fmaheavy pipe capacity: %d SMs x 4 SMSPs x 2 products/cycle x %.0f MHz "
+                                    "(IMAD.WIDE.U32 = 4 pipe cycles, 4 per product)" % (sms, mhz),
+                     "algorithmic_products_per_launch": prods, "avg_launch_ms": avg64, "ncu": pipe,
+                     "hbm": {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                             "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes64},
+                     "u01f_f32_launch_ms": avg32, "u01f_f32_achieved_gbs": 4.0 * N_HEAD / (avg32 / 1e3) / 1e9},
         "gpu_launches": 2 * args.steps,
         "clocks": clocks,
     }
@@ -320,11 +398,17 @@ def run_sharded(rank, world, dev, reps=3):
             "timing": "wall clock per rank around fill_sharded (host-synchronising protocol), max over ranks"}
 
 
-def run_per_config(dev, stream, sptr, buf, peak):
-    """Device-time Gsamples/s for the other BASELINE configs (3 timed reps each)."""
+def run_per_config(dev, stream, sptr, buf, peak, cpu_seconds, cpu=True):
+    """Every BASELINE row at its stated size, timed through the product call (Rng.fill with
+    a device `out`, fill_streams, Rng.mvn): CUDA events on the stream around the
+    synchronous call, best of 3 after a warm-up. Beside each: the fraction of the store-only
+    HBM figure (the ceiling of a fill) and of the copy figure, and the same-run
+    CPU rate of the port (P = all host threads, and P = 1)."""
     import torch
 
+    from oracle import oracle as O
     from paper_2605_05099_b200 import _lib, fill_streams, state_io
+    from paper_2605_05099_b200.rng import _out_dtype
 
     res = {}
     # store-only HBM figure of this box (SURVEY 8(d)): torch's fill_ over the 8 GiB buffer
@@ -338,94 +422,116 @@ def run_per_config(dev, stream, sptr, buf, peak):
         wbest = min(wbest, a.elapsed_time(z))
     wpeak = buf.numel() * 8 / (wbest / 1e3) / 1e9
     res["hbm_write_peak"] = {"gbs": wpeak, "how": "torch fill_ of an 8 GiB tensor, best of 6, CUDA events"}
+    P = O.cpu_count()
+    res["cpu"] = {"model": cpu_model(), "threads": P,
+                  "how": "oracle port (C restatement of the reference), P threads on disjoint substreams "
+                         "(philox counter offsets, x256 GF(2) jumps, pcg64 advance, ranlux A^k, sfc64 spawned "
+                         "streams), repeated fills of ~50 ms per call for %.1f s; and P = 1" % cpu_seconds}
 
-    def time_fill(label, engine, seed, dist, params, n, fm=False, reps=3, bytes_per=8):
-        r = state_io.create(engine, seed=seed)
-        r.set_full_mantissa(fm)
-        s = r.to_stream()
-        fp = r._continuous_params(dist, params, n) if dist not in ("uint64",) else []
-        fpa = (ctypes.c_double * 4)(*(list(fp) + [0.0] * (4 - len(fp))))
-        b = int(params.get("b", 0)) if dist == "uint64" else 0
-        ipa = _lib.u64_array([b, 0] if b != 1 << 64 else [0, 1], 4)
-        out = buf.view(torch.uint8)[: n * bytes_per]
-        did = _lib.DIST_IDS[dist]
-
-        def go():
-            _lib.check(_lib.lib.rs_fill_async(ctypes.byref(s), did, fpa, ipa, n, ctypes.c_void_p(out.data_ptr()),
-                                              sptr))
+    def timed(go, reps=3):
         go()
         torch.cuda.synchronize()
-        a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
+        best = 1e9
         for _ in range(reps):
+            a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
             go()
-        z.record(stream)
-        torch.cuda.synchronize()
-        ms = a.elapsed_time(z) / reps
-        gbs = n * bytes_per / (ms / 1e3) / 1e9
-        res[label] = {"gsamples_s": n / (ms / 1e3) / 1e9, "ms": ms, "n": n, "hbm_frac": gbs / peak,
-                      "write_frac": gbs / wpeak}
+            z.record(stream)
+            torch.cuda.synchronize()
+            best = min(best, a.elapsed_time(z))
+        return best
 
-    time_fill("c1_x256ss_raw_u64_2p30", "x256**", [12345], "uint64", {}, 1 << 30)
-    time_fill("c2_philox_u01_f64_2p30", "philox", [7], "u01", {}, 1 << 30, fm=True)
-    time_fill("c2_philox_u01f_f32_2p30", "philox", [7], "u01f", {}, 1 << 30, fm=True, bytes_per=4)
-    time_fill("c3_x256ss_norm_2p28", "x256**", [2024], "norm", {}, 1 << 28)
-    time_fill("c3_pcg64_norm_2p28", "pcg64", [2024], "norm", {}, 1 << 28)
-    time_fill("c4_pcg64_exp_2p26", "pcg64", [99], "exp", {}, 1 << 26)
+    def cpu_pair(engine, seed, dist, params, fm=False, spawn=False):
+        if not cpu:
+            return None
+        return {"p_all": cpu_rate(engine, seed, dist, params, P, cpu_seconds, fm, spawn),
+                "p_1": cpu_rate(engine, seed, dist, params, 1, cpu_seconds, fm, spawn)}
+
+    def row(label, engine, seed, dist, params, n, fm=False):
+        r = state_io.create(engine, seed=seed)
+        r.set_full_mantissa(fm)
+        out = buf.view(_out_dtype(dist))[:n]
+        ms = timed(lambda: r.fill(dist, params, n, out=out))
+        bpe = out.element_size()
+        gbs = n * bpe / (ms / 1e3) / 1e9
+        res[label] = {"gsamples_s": n / (ms / 1e3) / 1e9, "ms": ms, "n": n, "bytes_per_sample": bpe,
+                      "write_frac": gbs / wpeak, "hbm_frac": gbs / peak,
+                      "timed": "Rng.fill(dist, params, n, out=device tensor) -> rs_fill (synchronous)",
+                      "cpu": cpu_pair(engine, seed, dist, params, fm)}
+
+    row("c1_x256ss_raw_u64_2p30", "x256**", [12345], "uint64", {}, 1 << 30)
+    row("c2_philox_u01_f64_2p30", "philox", [7], "u01", {}, 1 << 30, fm=True)
+    row("c2_philox_u01f_f32_2p30", "philox", [7], "u01f", {}, 1 << 30, fm=True)
+    row("c3_x256ss_norm_2p28", "x256**", [2024], "norm", {}, 1 << 28)
+    row("c3_pcg64_norm_2p28", "pcg64", [2024], "norm", {}, 1 << 28)
+    row("c4_pcg64_exp_2p26", "pcg64", [99], "exp", {}, 1 << 26)
     for k in (0.3, 1.0, 2.5, 10.0):
-        time_fill("c4_pcg64_gamma_%g_2p26" % k, "pcg64", [99], "gamma", {"alpha": k}, 1 << 26)
-    time_fill("c4_pcg64_beta_2_5_2p26", "pcg64", [99], "beta", {"a": 2.0, "b": 5.0}, 1 << 26)
-    time_fill("extra_ranlux_raw_2p28", "ranlux++", [12345], "uint64", {}, 1 << 28, reps=2)
+        row("c4_pcg64_gamma_%g_2p26" % k, "pcg64", [99], "gamma", {"alpha": k}, 1 << 26)
+    row("c4_pcg64_beta_2_5_2p26", "pcg64", [99], "beta", {"a": 2.0, "b": 5.0}, 1 << 26)
+    row("extra_ranlux_raw_2p30", "ranlux++", [12345], "uint64", {}, 1 << 30)
     # C5b: sfc64 per-stream Lemire, 2^16 streams x 4096
+    S, per = 1 << 16, 4096
     for m in (6, 1000003, (1 << 63) + 1):
-        rows = fill_streams("sfc64", [31], [], 0, 1 << 16, "uint64", {"b": m}, 4096)
-        torch.cuda.synchronize()
-        a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(3):
-            fill_streams("sfc64", [31], [], 0, 1 << 16, "uint64", {"b": m}, 4096, out=rows)
-        z.record(stream)
-        torch.cuda.synchronize()
-        ms = a.elapsed_time(z) / 3
-        n = 1 << 28
-        res["c5b_sfc64_streams_lemire_%d_2p28" % m] = {"gsamples_s": n / (ms / 1e3) / 1e9, "ms": ms, "n": n,
-                                                       "hbm_frac": n * 8 / (ms / 1e3) / 1e9 / peak,
-                                                       "write_frac": n * 8 / (ms / 1e3) / 1e9 / wpeak,
-                                                       "note": "fill_streams(..., out=) into a resident 2 GiB tensor"}
-    # C5a: mvn (z fill + cuBLAS DGEMM), d in {64, 256, 512}, n = 2^20
+        rows = torch.empty((S, per), dtype=torch.uint64, device=dev)
+        ms = timed(lambda: fill_streams("sfc64", [31], [], 0, S, "uint64", {"b": m}, per, out=rows))
+        n = S * per
+        gbs = n * 8 / (ms / 1e3) / 1e9
+        res["c5b_sfc64_streams_lemire_%d_2p28" % m] = {
+            "gsamples_s": n / (ms / 1e3) / 1e9, "ms": ms, "n": n, "write_frac": gbs / wpeak, "hbm_frac": gbs / peak,
+            "timed": "fill_streams(..., out=) into a resident 2 GiB tensor -> rs_fill_streams",
+            "cpu": cpu_pair("sfc64", [31], "uint64", {"b": m}, spawn=True)}
+        del rows
+    # FP64 peak for the MVN contraction (SURVEY 8(d)): cuBLAS DGEMM 8192^3 through torch
+    mm = 8192
+    a64 = torch.randn(mm, mm, dtype=torch.float64, device=dev)
+    b64 = torch.randn(mm, mm, dtype=torch.float64, device=dev)
+    c64 = torch.matmul(a64, b64)
+    ms = timed(lambda: torch.matmul(a64, b64, out=c64))
+    tf = 2.0 * mm ** 3 / (ms / 1e3) / 1e12
+    res["fp64_dgemm_peak"] = {"tflops": tf, "how": "torch.matmul f64 8192^3 (cuBLAS DGEMM), best of 3, CUDA events"}
+    del a64, b64, c64
+    # C5a: mvn, d in {64, 256, 512}, n = 2^20 (the BASELINE recipe: philox seed 31, S from the
+    # same r, mvn on the same r). Whole call (z draw overlapping the host Cholesky, then the
+    # contraction) and the contraction alone (rs_mvn_apply: k_mvn_dmma, FP64 tensor cores)
     for d in (64, 256, 512):
+        n = 1 << 20
         r = state_io.create("philox", seed=[31])
         A = r.fill("norm", {}, d * d).cpu().numpy().reshape(d, d)
-        S = A @ A.T / d + np.eye(d)
-        r.mvn(np.zeros(d), S, n=1 << 20)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        r.mvn(np.zeros(d), S, n=1 << 20)
-        torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-        res["c5a_mvn_d%d_2p20" % d] = {"vectors_per_s": (1 << 20) / el, "ms": el * 1e3,
-                                        "gflops_dense": 2.0 * (1 << 20) * d * d / el / 1e9,
-                                        "gflops_triangular": 1.0 * (1 << 20) * d * (d + 1) / el / 1e9,
-                                        "note": "wall clock incl. host Cholesky and sync (rs_mvn is synchronous)"}
-    # FP64 peak for the MVN contraction (SURVEY 8(d)): cuBLAS DGEMM 8192^3 through torch
-    m = 8192
-    a64 = torch.randn(m, m, dtype=torch.float64, device=dev)
-    b64 = torch.randn(m, m, dtype=torch.float64, device=dev)
-    c64 = torch.matmul(a64, b64)
-    best = 1e9
-    for _ in range(3):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        torch.matmul(a64, b64, out=c64)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        best = min(best, e0.elapsed_time(e1))
-    tf = 2.0 * m ** 3 / (best / 1e3) / 1e12
-    res["fp64_dgemm_peak"] = {"tflops": tf, "how": "torch.matmul f64 8192^3 (cuBLAS DGEMM), best of 3, CUDA events"}
-    for d in (64, 256, 512):
-        row = res["c5a_mvn_d%d_2p20" % d]
-        row["dense_frac_of_dgemm"] = row["gflops_dense"] / 1e3 / tf
-    del a64, b64, c64
+        S_ = A @ A.T / d + np.eye(d)
+        ms_all = timed(lambda: r.mvn(np.zeros(d), S_, n=n), reps=2)
+        Lf = np.ascontiguousarray(np.linalg.cholesky(S_))
+        mean = np.zeros(d)
+        z = r.device_fill("stdnorm", [], [], n * d)
+        X = torch.empty(n * d, dtype=torch.float64, device=dev)
+        ms_k = timed(lambda: _lib.check(_lib.lib.rs_mvn_apply(
+            ctypes.c_void_p(Lf.ctypes.data), mean.ctypes.data_as(_lib.DBLP), d, n, 0, ctypes.c_void_p(z.data_ptr()),
+            ctypes.c_void_p(X.data_ptr()), sptr)))
+        del z, X
+        tri = n * d * (d + 1)
+        cpu_r = None
+        if cpu:  # the reference's CPU path: z by the port (P threads), X = z @ L^T by numpy
+            nn = 1 << 14
+            o = O.OracleRng("philox", seed=[31])
+            t0 = time.perf_counter()
+            reps = 0
+            while True:
+                zs = O.threaded_fill([o.clone() for _ in range(P)], "stdnorm", {}, nn * d // P)
+                zz = np.concatenate(zs).reshape(-1, d)
+                _ = zz @ Lf.T
+                reps += 1
+                el = time.perf_counter() - t0
+                if el >= cpu_seconds:
+                    break
+            cpu_r = {"vectors_per_s": reps * nn / el, "cores": P,
+                     "how": "z by the port on P threads + numpy z @ L^T (OpenBLAS), 2^14 vectors per call"}
+        res["c5a_mvn_d%d_2p20" % d] = {
+            "vectors_per_s": n / (ms_all / 1e3), "ms": ms_all,
+            "timed": "Rng.mvn(0, S, 2^20): z fill + host Cholesky (overlapped) + contraction",
+            "contraction_ms": ms_k, "contraction_tflops_triangular": tri / (ms_k / 1e3) / 1e12,
+            "contraction_tflops_dense_equiv": 2.0 * n * d * d / (ms_k / 1e3) / 1e12,
+            "contraction_frac_of_dgemm_peak": tri / (ms_k / 1e3) / 1e12 / tf,
+            "contraction_kernel": "k_mvn_dmma (mma.sync f64 / DMMA.8x8x4; triangular skip)",
+            "cpu": cpu_r}
     return res
 
 
@@ -439,19 +545,20 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        for _ in range(max(0, min(args.warmup, 1))):
-            cpu_reference(0.2)
-        vals = []
-        for _ in range(max(1, min(args.steps, 3))):
-            v, P, sample = cpu_reference(args.cpu_seconds)
-            vals.append(v)
-        v = float(np.median(vals))
+        ref = C2Reference(world)
+        for _ in range(args.warmup):
+            ref.step()
+        times = [ref.step() for _ in range(args.steps)]
+        el = float(np.sum(times))
+        v = 2 * N_HEAD * world * args.steps / el / 1e9
         line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-                "steps": len(vals), "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic: seeded stream fills",
-                "config": {"workload": "BASELINE config 2 (philox seed=7 full_mantissa, u01 f64 + u01f f32), "
-                                       "bounded CPU sample"},
-                "cpu_baseline": {"value": v, "unit": UNIT, "cores": P, "kind": "port", "sample": sample},
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
+                "data": "synthetic: seeded stream fills (no dataset is involved)",
+                "config": {"workload": "BASELINE config 2: philox (Philox-4x64-10) seed=7 full_mantissa; u01 f64 "
+                                       "n=2^30 + u01f f32 n=2^30 per GPU; rank g = counter-offset slice g",
+                           "same_config": True, "parallelism": "%d host threads" % ref.P},
+                "cpu_baseline": {"value": v, "unit": UNIT, "cores": ref.P, "kind": "port", "sample": ref.sample()},
                 "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return 0
@@ -464,9 +571,13 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     line = run_ours(args, rank, world, local_rank)
     if rank == 0:
-        if world == 1:
-            v, P, sample = cpu_reference(args.cpu_seconds)
-            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": P, "kind": "port", "sample": sample}
+        if world == 1 and not args.no_cpu:
+            ref = C2Reference(1)
+            ref.step()  # first touch of the host arrays
+            el = ref.step()
+            v = 2 * N_HEAD / el / 1e9
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": ref.P, "kind": "port",
+                                    "sample": ref.sample() + "; one timed step after one warm-up"}
         print(json.dumps(line))
     if world > 1:
         dist.barrier()

@@ -1008,7 +1008,7 @@ typedef struct { orc_rng r; int dist; double fp[4]; uint64_t ip[4]; uint64_t n; 
 static void *job_run(void *a) { job_t *j = (job_t *)a; orc_fill(&j->r, j->dist, j->fp, j->ip, j->n, j->out); return 0; }
 int orc_fill_threads(orc_rng *rs, int nthreads, int dist, const double *fp, const uint64_t *ip,
                      uint64_t n_per_thread, void **outs) {
-    pthread_t th[256];
+    pthread_t *th = (pthread_t *)calloc(nthreads, sizeof(pthread_t));
     job_t *jobs = (job_t *)calloc(nthreads, sizeof(job_t));
     for (int t = 0; t < nthreads; t++) {
         jobs[t].r = rs[t]; jobs[t].dist = dist; jobs[t].n = n_per_thread; jobs[t].out = outs[t];
@@ -1017,6 +1017,7 @@ int orc_fill_threads(orc_rng *rs, int nthreads, int dist, const double *fp, cons
     }
     for (int t = 0; t < nthreads; t++) { pthread_join(th[t], 0); rs[t] = jobs[t].r; }
     free(jobs);
+    free(th);
     return 0;
 }
 size_t orc_sizeof_rng(void) { return sizeof(orc_rng); }

@@ -304,14 +304,17 @@ def engine_generate(engine, state, n):
     return [int(v) for v in out], [int(s[i]) for i in range(STATE_WORDS[eid])]
 
 
-def threaded_fill(rngs, dist, params, n_per_thread):
-    """Run len(rngs) oracle streams on host threads (the CPU baseline leg)."""
+def threaded_fill(rngs, dist, params, n_per_thread, outs=None):
+    """Run len(rngs) oracle streams on host threads (the CPU baseline leg). `outs`: optional
+    preallocated per-thread output arrays (each >= n_per_thread elements of the law's dtype)."""
     L = lib()
     k = len(rngs)
     arr = (_Rng * k)()
     for i, r in enumerate(rngs):
         ctypes.memmove(ctypes.byref(arr[i]), ctypes.byref(r.r), ctypes.sizeof(_Rng))
-    outs = [np.empty(int(n_per_thread), dtype=out_dtype(dist)) for _ in range(k)]
+    if outs is None:
+        outs = [np.empty(int(n_per_thread), dtype=out_dtype(dist)) for _ in range(k)]
+    assert len(outs) == k and all(o.size >= n_per_thread and o.dtype == out_dtype(dist) for o in outs)
     ptrs = (ctypes.c_void_p * k)(*[o.ctypes.data for o in outs])
     fp = (ctypes.c_double * 4)(*fparams_for(dist, params))
     ip, _ = _u64arr(iparams_for(dist, params))

@@ -1,4 +1,4 @@
-// Serial single-stream kernels (no skip-ahead), the x256 jump setup and the MVN init.
+// Serial single-stream kernels (no skip-ahead) and the x256 jump setup.
 #define RS_KERNELS_MISC
 #include "rs_kernels.cuh"
 
@@ -23,4 +23,3 @@ const void *rsk::serial_kernel(int engine, int fam, int fixed_mode) {
                                        : serial_e<RS_ENG_SFC64>(fam, fixed_mode);
 }
 const void *rsk::setup_kernel() { return (const void *)k_x256_setup; }
-const void *rsk::mvn_init_kernel() { return (const void *)k_mvn_init; }

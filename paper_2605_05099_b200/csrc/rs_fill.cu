@@ -58,7 +58,6 @@ struct DevCtx {
     std::map<std::tuple<int, u64, int>, u64 *> x256_ml;  // (family, L, levels) -> matrices
     void *stage = nullptr;
     size_t stage_bytes = 0;
-    cublasHandle_t blas = nullptr;
     double *mvn_z = nullptr;
     size_t mvn_bytes = 0;
     u64 *words = nullptr;  // materialized engine words for parse-from-memory
@@ -906,6 +905,21 @@ void tally_seen(const Resolved &r, int32_t *seen) {
     if (r.family == FAM_GAMMA) { seen[0] = 1; seen[2] = 1; }
 }
 
+// Restores the caller's current device on every return path: the entry points switch to
+// the output pointer's device, and a Python caller's torch current device must not move.
+struct DeviceGuard {
+    int prev = -1;
+    DeviceGuard() {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            cudaGetLastError();
+            prev = -1;
+        }
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 rs_status check_stream(const rs_stream *s) {
     if (!s) { rs::set_error("null stream"); return RS_ERR_VALUE; }
     if (!rs::device_engine(s->engine)) { rs::set_error("engine not on the B200 fill path"); return RS_ERR_UNSUPPORTED; }
@@ -923,6 +937,7 @@ extern "C" {
 
 rs_status rs_init_device(int32_t device) {
     std::lock_guard<std::mutex> g(g_mu);
+    DeviceGuard dg;
     CK(cudaSetDevice(device));
     DevCtx *c;
     rs_status s = init_dev(device, &c);
@@ -930,9 +945,10 @@ rs_status rs_init_device(int32_t device) {
     return s;
 }
 
-rs_status rs_fill(rs_stream *s, int32_t dist, const double *fparams, const uint64_t *iparams, uint64_t n, void *out,
-                  rs_fill_result *result, void *cuda_stream) {
-    std::lock_guard<std::mutex> g(g_mu);
+// rs_fill with g_mu already held by the caller (rs_fill, mvn_core)
+static rs_status fill_locked(rs_stream *s, int32_t dist, const double *fparams, const uint64_t *iparams, uint64_t n,
+                             void *out, rs_fill_result *result, void *cuda_stream) {
+    DeviceGuard dg;
     rs_status rc = check_stream(s);
     if (rc) return rc;
     double fz[4] = {0, 0, 0, 0};
@@ -1002,6 +1018,12 @@ rs_status rs_fill(rs_stream *s, int32_t dist, const double *fparams, const uint6
     return RS_OK;
 }
 
+rs_status rs_fill(rs_stream *s, int32_t dist, const double *fparams, const uint64_t *iparams, uint64_t n, void *out,
+                  rs_fill_result *result, void *cuda_stream) {
+    std::lock_guard<std::mutex> g(g_mu);
+    return fill_locked(s, dist, fparams, iparams, n, out, result, cuda_stream);
+}
+
 rs_status rs_fill_async(const rs_stream *s, int32_t dist, const double *fparams, const uint64_t *iparams, uint64_t n,
                         void *out_device, void *cuda_stream) {
     std::lock_guard<std::mutex> g(g_mu);
@@ -1012,6 +1034,12 @@ rs_status rs_fill_async(const rs_stream *s, int32_t dist, const double *fparams,
     Resolved r;
     rc = resolve(dist, fparams ? fparams : fz, iparams ? iparams : iz, r);
     if (rc) return rc;
+    // A variable-consumption fill needs host round trips (the resolution flag, further
+    // fixup rounds, a second provisioning chunk, the overrun check): rs_fill only.
+    if (r.fixed_mode < 0 || is_serial(s->engine)) {
+        rs::set_error("rs_fill_async covers fixed-consumption laws on skip-ahead engines; use rs_fill");
+        return RS_ERR_UNSUPPORTED;
+    }
     if (n == 0) return RS_OK;
     int dev;
     CK(cudaGetDevice(&dev));
@@ -1029,6 +1057,7 @@ rs_status rs_fill_streams(int32_t engine, const uint64_t *seed, int32_t n_seed, 
                           int32_t n_prefix, uint64_t j0, uint64_t n_streams, int32_t dist, const double *fparams,
                           const uint64_t *iparams, uint64_t n_per_stream, void *out, void *cuda_stream) {
     std::lock_guard<std::mutex> g(g_mu);
+    DeviceGuard dg;
     if (engine != RS_ENG_SFC64 && engine != RS_ENG_PCG64 && engine != RS_ENG_PHILOX && engine != RS_ENG_X256SS &&
         engine != RS_ENG_X256PP && engine != RS_ENG_X128P && engine != RS_ENG_XORO && engine != RS_ENG_SQUARES &&
         engine != RS_ENG_CHACHA20 && engine != RS_ENG_CWG128) {
@@ -1119,61 +1148,56 @@ rs_status rs_fill_streams(int32_t engine, const uint64_t *seed, int32_t n_seed, 
     return RS_OK;
 }
 
-// rs_mvn (zext == nullptr: z drawn here from `s`) and rs_mvn_apply (z given, on the device)
+// rs_mvn (zext == nullptr: z drawn here from `s`) and rs_mvn_apply (z given, on the device).
+// One lock from the scratch sizing to the final synchronisation: the per-device scratch
+// (z, the factor, the mean, the staging buffer) is shared by every caller on the device.
 static rs_status mvn_core(rs_stream *s, const double *L, const double *mean, int64_t d, uint64_t n, int32_t layout,
                           const double *zext, double *out, rs_fill_result *result, void *cuda_stream) {
     if (d < 1 || n < 1) { rs::set_error("mvn needs n >= 1"); return RS_ERR_VALUE; }
     if (layout != 0 && layout != 1) { rs::set_error("mvn layout must be 'n_d' or 'd_n'"); return RS_ERR_VALUE; }
+    if (d > (1 << 20)) { rs::set_error("mvn dimension too large"); return RS_ERR_VALUE; }
+    std::lock_guard<std::mutex> g(g_mu);
+    DeviceGuard dg;
     rs_status rc;
+    if (!zext && (rc = check_stream(s))) return rc;
+    if (zext && !is_device_ptr(zext)) { rs::set_error("mvn z must be device memory"); return RS_ERR_VALUE; }
     int dev;
-    {
-        std::lock_guard<std::mutex> g(g_mu);
-        if (!zext && (rc = check_stream(s))) return rc;
-        if (zext && !is_device_ptr(zext)) { rs::set_error("mvn z must be device memory"); return RS_ERR_VALUE; }
-        if (is_device_ptr(out)) {
-            cudaPointerAttributes a;
-            CK(cudaPointerGetAttributes(&a, out));
-            dev = a.device;
-            CK(cudaSetDevice(dev));
-        } else {
-            CK(cudaGetDevice(&dev));
-        }
+    if (is_device_ptr(out)) {
+        cudaPointerAttributes a;
+        CK(cudaPointerGetAttributes(&a, out));
+        dev = a.device;
+        CK(cudaSetDevice(dev));
+    } else {
+        CK(cudaGetDevice(&dev));
     }
     DevCtx *c;
-    {
-        std::lock_guard<std::mutex> g(g_mu);
-        if ((rc = init_dev(dev, &c))) return rc;
-    }
+    if ((rc = init_dev(dev, &c))) return rc;
     cudaStream_t st = (cudaStream_t)cuda_stream;
-    size_t nz = (size_t)n * (size_t)d;
-    // z and the factor / mean in device memory
-    size_t need = (zext ? 0 : nz * 8) + (size_t)d * d * 8 + (size_t)d * 8;
-    {
-        std::lock_guard<std::mutex> g(g_mu);
-        if (need > c->mvn_bytes) {
-            cudaFree(c->mvn_z);
-            c->mvn_z = nullptr;
-            CK(cudaMalloc(&c->mvn_z, need));
-            c->mvn_bytes = need;
-        }
-        if (!c->blas) {
-            if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) { rs::set_error("cublasCreate failed"); return RS_ERR_CUDA; }
-        }
+    const size_t nz = (size_t)n * (size_t)d;
+    // z (unless given), the factor and the mean in device memory; offsets keep 16-byte alignment
+    const size_t zb = zext ? 0 : (nz * 8 + 15) / 16 * 16, lb = ((size_t)d * d * 8 + 15) / 16 * 16;
+    const size_t need = zb + lb + (size_t)d * 8;
+    if (need > c->mvn_bytes) {
+        cudaFree(c->mvn_z);
+        c->mvn_z = nullptr;
+        c->mvn_bytes = 0;
+        CK(cudaMalloc(&c->mvn_z, need));
+        c->mvn_bytes = need;
     }
-    double *zbuf = c->mvn_z, *Ld = zbuf + (zext ? 0 : nz), *md = Ld + (size_t)d * d;
+    double *zbuf = c->mvn_z, *Ld = (double *)((char *)c->mvn_z + zb), *md = (double *)((char *)c->mvn_z + zb + lb);
     const double *z = zext ? zext : zbuf;
     CK(cudaMemcpyAsync(Ld, L, (size_t)d * d * 8, cudaMemcpyDefault, st));
     CK(cudaMemcpyAsync(md, mean, (size_t)d * 8, cudaMemcpyDefault, st));
     rs_fill_result fr;
     memset(&fr, 0, sizeof fr);
-    if (!zext && (rc = rs_fill(s, RS_DIST_STDNORM, nullptr, nullptr, nz, zbuf, &fr, cuda_stream))) return rc;
-    std::lock_guard<std::mutex> g(g_mu);
-    bool host_out = !is_device_ptr(out);
+    if (!zext && (rc = fill_locked(s, RS_DIST_STDNORM, nullptr, nullptr, nz, zbuf, &fr, cuda_stream))) return rc;
+    const bool host_out = !is_device_ptr(out);
     double *X;
     if (host_out) {
         if (nz * 8 > c->stage_bytes) {
             cudaFree(c->stage);
             c->stage = nullptr;
+            c->stage_bytes = 0;
             CK(cudaMalloc(&c->stage, nz * 8));
             c->stage_bytes = nz * 8;
         }
@@ -1181,14 +1205,10 @@ static rs_status mvn_core(rs_stream *s, const double *L, const double *mean, int
     } else {
         X = out;
     }
-    u64 nn = n;
-    const unsigned ig = (unsigned)std::min<u64>((nz + 255) / 256, 148 * 16);
-    cublasSetStream(c->blas, st);
-    double one = 1.0;
-    cublasStatus_t bs;
-    // a Cholesky factor is lower triangular; the pivoted semidefinite factor is not
-    // (continuous.py:293-309), and takes the dense GEMM
-    bool lower = true;
+    // A Cholesky factor is lower triangular (exact zeros above the diagonal): the kernel
+    // skips the zero products. The pivoted semidefinite factor (continuous.py:293-309) is
+    // not, and takes the full product.
+    int lower = 1;
     {
         std::vector<double> hl;
         const double *Lh = L;
@@ -1200,53 +1220,25 @@ static rs_status mvn_core(rs_stream *s, const double *L, const double *mean, int
         }
         for (int64_t r = 0; r < d && lower; r++)
             for (int64_t q = r + 1; q < d; q++)
-                if (Lh[r * d + q] != 0.0) { lower = false; break; }
+                if (Lh[r * d + q] != 0.0) { lower = 0; break; }
     }
-    // (below d ~ 200 the DGEMM is faster than cuBLAS's TRMM on B200: d = 64 1.70 vs 1.82 ms)
-    if (layout == 0 && lower && d >= 192) {
-        // X (n x d row-major) = (d x n col-major) C = L * z^T. L is lower triangular, so a
-        // TRMM does the d(d+1)/2 nonzero products per vector, half the DGEMM's d^2: the
-        // L buffer (row-major L) is col-major L^T, upper, used transposed; B = z^T.
-        bs = cublasDtrmm(c->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)d,
-                         (int)n, &one, Ld, (int)d, z, (int)d, X, (int)d);
-        if (bs != CUBLAS_STATUS_SUCCESS) { rs::set_error("cublasDtrmm failed"); return RS_ERR_CUDA; }
-        // mean + C: one more pass over X (d = 512, n = 2^20: 1.6 ms), skipped for a zero mean,
-        // where it could only turn a -0.0 into +0.0 (equal values; MVN parity is the 1e-12
-        // tolerance of SURVEY 8(d), DGEMM-level results being unpinned by the reference)
-        bool zero_mean = true;
-        {
-            std::vector<double> hm;
-            const double *mh = mean;
-            if (is_device_ptr(mean)) {
-                hm.resize((size_t)d);
-                CK(cudaMemcpyAsync(hm.data(), mean, (size_t)d * 8, cudaMemcpyDeviceToHost, st));
-                CK(cudaStreamSynchronize(st));
-                mh = hm.data();
-            }
-            for (int64_t i = 0; i < d && zero_mean; i++) zero_mean = mh[i] == 0.0;
-        }
-        if (!zero_mean) {
-            int add = 1;
-            void *ia[] = {&X, &md, &d, &nn, &layout, &add};
-            if ((rc = launch(rsk::mvn_init_kernel(), dim3(ig), dim3(256), ia, st))) return rc;
-        }
-    } else {
-        int add = 0;
-        void *ia[] = {&X, &md, &d, &nn, &layout, &add};
-        if ((rc = launch(rsk::mvn_init_kernel(), dim3(ig), dim3(256), ia, st))) return rc;
-        if (layout == 0) {
-            // X (n x d row-major) = (d x n col-major) C = L * z^T : A = L buffer (row-major => col-major L^T), op T
-            bs = cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)d, (int)n, (int)d, &one, Ld, (int)d, z, (int)d,
-                             &one, X, (int)d);
-        } else {
-            // X^T (d x n row-major) = (n x d col-major) C = z * L^T : z buffer is (d x n) col-major -> op T
-            bs = cublasDgemm(c->blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)n, (int)d, (int)d, &one, z, (int)d, Ld, (int)d,
-                             &one, X, (int)n);
-        }
+    // 16-byte copies need an even d (rows 16-byte aligned) and aligned bases
+    const bool vec16 = d % 2 == 0 && (((uintptr_t)z | (uintptr_t)Ld | (uintptr_t)X) & 15) == 0;
+    rsk::MvnLaunch ml = rsk::mvn_kernel(vec16 ? 1 : 0, layout);
+    CK(cudaFuncSetAttribute(ml.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ml.smem));
+    {
+        long long nn = (long long)n;
+        int dd = (int)d;
+        int ntn = (dd + ml.bn - 1) / ml.bn;
+        unsigned long long blocks = (unsigned long long)((n + ml.bm - 1) / ml.bm) * (unsigned long long)ntn;
+        if (blocks > 0x7FFFFFFFULL) { rs::set_error("mvn too large for one launch"); return RS_ERR_VALUE; }
+        const double *zp = z, *lp = Ld, *mp = md;
+        void *args[] = {&zp, &lp, &mp, &X, &nn, &dd, &lower, &ntn};
+        if ((rc = launch(ml.fn, dim3((unsigned)blocks), dim3(ml.threads), args, st, ml.smem))) return rc;
     }
-    if (bs != CUBLAS_STATUS_SUCCESS) { rs::set_error("cublasDgemm failed"); return RS_ERR_CUDA; }
     if (host_out) CK(cudaMemcpyAsync(out, X, nz * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
     if (result) *result = fr;
     rs::clear_error();
     return RS_OK;

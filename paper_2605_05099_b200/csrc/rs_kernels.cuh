@@ -5,7 +5,6 @@
 // ~240 kernels compile in parallel.
 #pragma once
 #include <cuda_runtime.h>
-#include <cublas_v2.h>
 
 #include <type_traits>
 #include <cmath>
@@ -1782,20 +1781,6 @@ __global__ void __launch_bounds__(STR_BLOCK) k_streams(const __grid_constant__ S
     wr.finish();
 }
 
-#ifdef RS_KERNELS_MISC
-// layout n_d: C is d x n col-major => element i belongs to row i % d
-// layout d_n: C is n x d col-major => element i belongs to column i / n
-// add = 0: C = mean (before a beta = 1 GEMM); add = 1: C = mean + C (after the TRMM),
-// the reference's `mean + z @ factor.T` (continuous.py:331-336)
-__global__ void k_mvn_init(double *c, const double *mean, int64_t d, u64 n, int layout, int add) {
-    u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-    u64 tot = n * (u64)d;
-    for (; i < tot; i += (u64)gridDim.x * blockDim.x) {
-        double m = layout == 0 ? mean[i % d] : mean[i / n];
-        c[i] = add ? m + c[i] : m;
-    }
-}
-#endif  // RS_KERNELS_MISC
 
 }  // namespace
 
@@ -1815,5 +1800,10 @@ const void *streams_kernel(int engine, int fam); // k_streams_a.cu (dispatch), k
 const void *streams_kernel_b(int engine, int fam);
 const void *serial_kernel(int engine, int fam, int fixed_mode);  // k_misc.cu
 const void *setup_kernel();     // k_misc.cu: k_x256_setup
-const void *mvn_init_kernel();  // k_misc.cu: k_mvn_init
+struct MvnLaunch {  // k_mvn.cu: the FP64 tensor-core contraction X = mean + z L^T
+    const void *fn;
+    size_t smem;
+    int threads, bm, bn;
+};
+MvnLaunch mvn_kernel(int vec16, int layout);
 }  // namespace rsk

@@ -107,6 +107,10 @@ def _out_dtype(dist):
     return torch.float64
 
 
+_NP_OUT = {torch.uint64: np.dtype(np.uint64), torch.float32: np.dtype(np.float32), torch.uint32: np.dtype(np.uint32),
+           torch.int32: np.dtype(np.int32), torch.int64: np.dtype(np.int64), torch.float64: np.dtype(np.float64)}
+
+
 class Rng:
     def __init__(self, engine):
         self.engine = engine
@@ -304,13 +308,21 @@ class Rng:
         if out is None:
             dev = self._device()
             out = torch.empty(n, dtype=_out_dtype(dist), device=dev)
+        # rs_fill writes n * (the law's element size) bytes: the caller's buffer must hold
+        # exactly that element type, or the fill would run past its end
+        want = _out_dtype(dist)
         if isinstance(out, torch.Tensor):
+            if out.dtype != want:
+                raise ValueError("out must have dtype %s for %s (got %s)" % (want, dist, out.dtype))
             if out.numel() < n or not out.is_contiguous():
                 raise ValueError("out must be a contiguous tensor with at least n elements")
             ptr = out.data_ptr()
             stream = _cuda_stream_ptr(out.device) if out.is_cuda else ctypes.c_void_p(0)
         else:  # numpy host array (the e2e path: the library stages through device memory)
             arr = out
+            want_np = _NP_OUT[want]
+            if not isinstance(arr, np.ndarray) or arr.dtype.newbyteorder("=") != want_np:
+                raise ValueError("out must be a numpy array of dtype %s for %s" % (np.dtype(want_np), dist))
             if arr.size < n or not arr.flags["C_CONTIGUOUS"]:
                 raise ValueError("out must be a contiguous array with at least n elements")
             ptr = arr.ctypes.data

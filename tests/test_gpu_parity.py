@@ -401,6 +401,108 @@ def test_philox_counter_words(ctr, dist):
     _assert_same_position(r, o)
 
 
+@pytest.mark.parametrize("dist,n", [("u01", (1 << 16) + 5), ("u01f", (1 << 16) + 7), ("uint64", 4096 + 1)])
+@pytest.mark.parametrize("wrap", [0, 1])
+def test_philox_fold_boundary(dist, n, wrap):
+    """The fold/no-fold switch of k_philox_fixed at its exact boundary: with a buffered
+    prefix of P words, the launch's nblk blocks end at counter word 0 = 2^64 - 1
+    (wrap 0: no carry, folded rounds) or cross it by exactly one block (wrap 1: the
+    general loop). counter.py:98-121."""
+    pre = 5  # next_u64 x5: one refill (36 blocks), then P = 139 buffered words
+    P = 144 - pre
+    words = n if dist != "u01f" else (n + 1) // 2
+    nblk = (words - P + 3) // 4
+    o = O.OracleRng("philox", seed=[3])
+    ctr0 = (2 ** 64 - nblk + wrap - 36) % 2 ** 64  # the state after the refill is ctr0 + 36
+    st = [ctr0, 0xFFFFFFFFFFFFFFFF, 12345, 6789] + o.get_state()[4:]
+    r = state_io.create("philox", seed=[3])
+    r.set_state(st)
+    o.set_state(st)
+    r.set_full_mantissa(True)
+    o.set_full_mantissa(True)
+    for _ in range(pre):
+        assert r.next_u64() == o.next_u64()
+    assert r.to_stream().fill - r.to_stream().cursor == P
+    got = _np(r.fill(dist, {}, n))
+    assert np.array_equal(_bits(got), _bits(o.fill(dist, {}, n)))
+    _assert_same_position(r, o)
+
+
+def _chunks_vs_sequential_oracle(t, o, dist, params, chunk=1 << 26):
+    """Whole-array compare of a device fill against the sequential oracle, chunk by chunk
+    (fill(a) then fill(b) draws exactly fill(a + b) for these one-unit laws)."""
+    n = t.numel()
+    for off in range(0, n, chunk):
+        m = min(chunk, n - off)
+        ref = o.fill(dist, params, m)
+        got = t[off:off + m].cpu().numpy()
+        diff = np.nonzero(_bits(got) != _bits(ref))[0]
+        assert len(diff) == 0, (dist, "first diff at %d" % (off + diff[0]))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("dist", ["u01", "u01f"])
+def test_c2_full_2p30_whole(dist):
+    """BASELINE config 2 at its full size, every element: philox seed 7, full mantissa,
+    2^30 samples (counter.py:98-121, rng.py:98-115), plus the final position."""
+    n = 1 << 30
+    r = state_io.create("philox", seed=[7])
+    r.set_full_mantissa(True)
+    t = r.fill(dist, {}, n)
+    o = O.OracleRng("philox", seed=[7], full_mantissa=True)
+    _chunks_vs_sequential_oracle(t, o, dist, {})
+    _assert_same_position(r, o)
+    del t
+
+
+@pytest.mark.slow
+def test_ranlux_full_2p30_whole():
+    """The ranlux++ raw 2^30 extra config, every word (ranlux.py:36-88) and the final
+    position (A^(offset/9) skip-ahead per thread, ranlux.py:90-93)."""
+    n = 1 << 30
+    r = state_io.create("ranlux++", seed=[12345])
+    t = r.fill("uint64", {}, n)
+    o = O.OracleRng("ranlux++", seed=[12345])
+    _chunks_vs_sequential_oracle(t, o, "uint64", {})
+    _assert_same_position(r, o)
+    del t
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("d", [64, 256, 512])
+@pytest.mark.parametrize("layout", ["n_d", "d_n"])
+def test_c5a_mvn_baseline(d, layout):
+    """BASELINE config 5a exactly: r = create("philox", [31]); A from
+    r.fill("norm", d*d); S = A A^T / d + I; X = r.mvn(0, S, 2^20) on the SAME r
+    (z starts mid-buffer). z bit-exact vs the oracle, X within the north star's
+    1e-12 normwise bar (continuous.py:312-336), final position exact."""
+    n = 1 << 20
+    r = state_io.create("philox", seed=[31])
+    o = O.OracleRng("philox", seed=[31])
+    A = _np(r.fill("norm", {}, d * d))
+    assert np.array_equal(_bits(A), _bits(o.fill("norm", {}, d * d)))
+    A = A.reshape(d, d)
+    S = A @ A.T / d + np.eye(d)
+    L = np.linalg.cholesky(S)
+    zr = r.duplicate()  # the z draws of the mvn below, through the same device fill path
+    X = r.mvn(np.zeros(d), S, n=n, layout=layout)
+    zg = zr.device_fill("stdnorm", [], [], n * d)
+    rows = 1 << 16
+    worst = 0.0
+    for a in range(0, n, rows):
+        z = o.fill("stdnorm", {}, rows * d)
+        assert np.array_equal(_bits(zg[a * d:(a + rows) * d].cpu().numpy()), _bits(z)), a
+        z = z.reshape(rows, d)
+        ref = z @ L.T
+        got = (X[a:a + rows] if layout == "n_d" else X[:, a:a + rows].T).cpu().numpy()
+        scale = np.abs(z) @ np.abs(L).T
+        worst = max(worst, float(np.max(np.abs(got - ref) / scale)))
+    assert worst <= 1e-12, worst  # tolerance stated by the north star (SURVEY 8(d))
+    _assert_same_position(r, o)
+    _assert_same_position(zr, o)
+    del X, zg
+
+
 @pytest.mark.slow
 def test_c2_full_2p30_windows():
     n = 1 << 30
@@ -473,12 +575,14 @@ def _full_vs_oracle(engine, seed, dist, params, n):
 @pytest.mark.parametrize("m", [6, 1000003, (1 << 63) + 1])
 def test_c5b_full_2p28(m):
     S = 1 << 16
-    out = fill_streams("sfc64", [31], [], 0, S, "uint64", {"b": m}, (1 << 28) // S)
-    rows = np.random.default_rng(5).integers(0, S, 24)
+    per = (1 << 28) // S
+    out = fill_streams("sfc64", [31], [], 0, S, "uint64", {"b": m}, per)
     host = out.cpu().numpy()
-    for j in rows:
-        o = O.OracleRng("sfc64", seed=[31], spawn_key=(int(j),))
-        assert np.array_equal(host[j], o.fill("uint64", {"b": m}, (1 << 28) // S)), j
+    # every one of the 65,536 rows against its own oracle stream, 256 host threads at a time
+    for j0 in range(0, S, 256):
+        rngs = [O.OracleRng("sfc64", seed=[31], spawn_key=(j,)) for j in range(j0, j0 + 256)]
+        refs = O.threaded_fill(rngs, "uint64", {"b": m}, per)
+        assert np.array_equal(host[j0:j0 + 256], np.stack(refs)), j0
 
 
 @pytest.mark.parametrize("engine", ["x256**", "philox", "pcg64", "x256++simd"])

@@ -278,3 +278,25 @@ def test_range_abi_validates_before_touching_a_device():
     assert "fresh" in _lib.last_error()
     s = state_io.create("sfc64", seed=[1])                          # no skip-ahead
     assert call(s, "norm", 0, 144, 256) == _lib.RS_ERR_UNSUPPORTED
+
+
+REF_SRC = pathlib.Path("/root/reference/pkg/src")
+
+
+@pytest.mark.skipif(not (REF_SRC / "randstream" / "zigtables.py").exists(),
+                    reason="the reference is only in the build container")
+def test_tables_header_matches_reference_zigtables():
+    """csrc/rs_tables.h (used by the kernels AND the oracle) is exactly what
+    tools/gen_tables.py renders from the reference's zigtables.py: a stale table
+    cannot move the product and its checker together unnoticed."""
+    import runpy
+    import sys
+
+    argv = sys.argv
+    sys.argv = ["gen_tables.py", str(REF_SRC)]
+    try:
+        g = runpy.run_path(str(ROOT / "tools" / "gen_tables.py"), run_name="gen_tables")
+    finally:
+        sys.argv = argv
+    text = (ROOT / "paper_2605_05099_b200" / "csrc" / "rs_tables.h").read_text()
+    assert g["render"]() == text
