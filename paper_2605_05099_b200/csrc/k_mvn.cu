@@ -7,12 +7,14 @@
 // A = z (row-major M x K), B[c][r] = L[r][c] -- i.e. B "column-major" is L itself, rows
 // of L contiguous along K, exactly what mma.sync .row.col wants for both operands.
 //
-//  * mma.sync.m16n8k8 .f64 (SASS DMMA.8x8x4, the FP64 tensor pipe). Block tile 128 x 64
-//    (4 warps, 2 x 2, warp tile 64 x 32 = 4 x 4 mma tiles), K staged 16 at a time through
-//    a 4-deep cp.async pipeline (24 KB per stage, 2 blocks per SM).
-//  * The mma's k index is permuted inside each group of 8: logical k = t and t + 4 of
-//    thread t read physical k = 2t and 2t + 1, for A and B alike. The dot product is the
-//    same set of products, and each thread's pair of operands is one 16-byte LDS.128.
+//  * mma.sync.m8n8k4 .f64 = one DMMA.8x8x4 (the FP64 tensor pipe). Block tile 128 x 64
+//    (4 warps, 2 x 2, warp tile 64 x 32 = 8 x 4 tiles), K staged 16 at a time through a
+//    4-deep cp.async pipeline (24 KB per stage, 2 blocks per SM). The 32 DMMAs of a k4 step
+//    are independent; the next step's DMMA on the same accumulator comes 32 issues later
+//    (m16n8k8 chained two dependent DMMAs per tile: ncu showed "wait" as the top stall).
+//  * k is permuted inside each group of 8: the first k4 step takes physical k = 2t from
+//    thread t, the second 2t + 1, for A and B alike. The dot product is the same set of
+//    products, and each thread's pair of operands is one 16-byte LDS.128.
 //    Rows of a stage are 128 B; chunk c of row r sits at c ^ 4 (r & 1), so the 8 lanes of
 //    a quarter-warp (rows g, g + 1) hit 8 distinct 16-byte bank groups.
 //  * Lower-triangular L: L[r][c] = 0 for c > r, so the block for columns [n0, n0 + 64)
@@ -47,13 +49,11 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 // element (row r, col k) of a [rows][MV_BK] stage tile with the 16-byte-chunk swizzle
 __device__ __forceinline__ int sw(int r, int k) { return r * MV_BK + ((((k >> 1) ^ ((r & 1) << 2))) << 1) + (k & 1); }
 
-__device__ __forceinline__ void mma_k8(double (&c)[4], const double2 &a_lo, const double2 &a_hi, const double2 &b) {
-    // a0 = A[g][t] a1 = A[g+8][t] a2 = A[g][t+4] a3 = A[g+8][t+4]; b0 = B[t][g] b1 = B[t+4][g]
-    // with logical k = t -> physical 2t, t + 4 -> 2t + 1 (.x / .y of each pair)
-    asm volatile(
-        "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-        : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
-        : "d"(a_lo.x), "d"(a_hi.x), "d"(a_lo.y), "d"(a_hi.y), "d"(b.x), "d"(b.y));
+// one DMMA.8x8x4: c0, c1 = C[g][2t], C[g][2t+1] += sum_k A[g][k] B[k][2t..2t+1], thread t
+// supplying A[g][k_t] and B[k_t][g] for its k slot
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
 }
 
 // V: doubles per cp.async (2 when d is even and the pointers 16-byte aligned, else 1).
@@ -93,20 +93,19 @@ __global__ void __launch_bounds__(MV_THREADS, 2) k_mvn_dmma(const double *__rest
         }
     };
 
-    double acc[4][4][4];
+    // warp tile 64 x 32 = 8 x 4 tiles of 8 x 8; acc[i][j] = C[8i + g][8j + 2t, +1]
+    double acc[8][4][2];
 #pragma unroll
-    for (int i = 0; i < 4; i++)
+    for (int i = 0; i < 8; i++)
 #pragma unroll
-        for (int j = 0; j < 4; j++)
-#pragma unroll
-            for (int q = 0; q < 4; q++) acc[i][j][q] = 0.0;
+        for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
     for (int s = 0; s < MV_STAGES - 1; s++) {
         if (s < ktiles) load_stage(s, s);
         cp_commit();
     }
-    // the last column of each of this warp's 8-column mma tiles (triangular skip)
+    // the first column of this warp's tiles (triangular skip: tile j needs k < wcol + 8 j + 8)
     const int wcol = n0 + 32 * wn;
     for (int kt = 0; kt < ktiles; kt++) {
         cp_wait<MV_STAGES - 2>();
@@ -120,25 +119,33 @@ __global__ void __launch_bounds__(MV_THREADS, 2) k_mvn_dmma(const double *__rest
         const double *sb = sa + MV_BM * MV_BK;
 #pragma unroll
         for (int ks = 0; ks < MV_BK / 8; ks++) {
-            const int kg = kt * MV_BK + 8 * ks;  // global k of this k8 step
+            const int kg = kt * MV_BK + 8 * ks;  // global k of this group of 8
             const int kk = 8 * ks + 2 * t;       // this thread's physical k pair in the stage
-            double2 b[4];
+            // each k8 group runs as two k4 DMMA steps: step 0 takes physical k = 2t (.x),
+            // step 1 k = 2t + 1 (.y) -- one LDS.128 per operand pair, and the 32 tiles of a
+            // step are independent, so no DMMA waits on the previous one's accumulator
+            double2 b[4], a[8];
 #pragma unroll
             for (int j = 0; j < 4; j++) b[j] = *(const double2 *)(sb + sw(32 * wn + 8 * j + g, kk));
 #pragma unroll
-            for (int i = 0; i < 4; i++) {
-                const int r = 64 * wm + 16 * i + g;
-                const double2 alo = *(const double2 *)(sa + sw(r, kk));
-                const double2 ahi = *(const double2 *)(sa + sw(r + 8, kk));
+            for (int i = 0; i < 8; i++) a[i] = *(const double2 *)(sa + sw(64 * wm + 8 * i + g, kk));
 #pragma unroll
-                for (int j = 0; j < 4; j++)
-                    if (!lower || kg < wcol + 8 * j + 8) mma_k8(acc[i][j], alo, ahi, b[j]);
+            for (int j = 0; j < 4; j++) {
+                if (lower && kg >= wcol + 8 * j + 8) continue;  // warp-uniform: L[r][c] = 0 for c > r
+#pragma unroll
+                for (int i = 0; i < 8; i++) dmma(acc[i][j], a[i].x, b[j].x);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                if (lower && kg >= wcol + 8 * j + 8) continue;
+#pragma unroll
+                for (int i = 0; i < 8; i++) dmma(acc[i][j], a[i].y, b[j].y);
             }
         }
     }
     cp_wait<0>();
 
-    // epilogue: c0, c1 = C[g][2t, 2t+1]; c2, c3 = C[g+8][2t, 2t+1]
+    // epilogue: acc[i][j] = C[8i + g][8j + 2t, 8j + 2t + 1] (+ mean), 16-byte stores (n_d)
 #pragma unroll
     for (int j = 0; j < 4; j++) {
         const int col = n0 + 32 * wn + 8 * j + 2 * t;
@@ -146,24 +153,21 @@ __global__ void __launch_bounds__(MV_THREADS, 2) k_mvn_dmma(const double *__rest
         const bool two = col + 1 < d;
         const double mu0 = __ldg(mean + col), mu1 = two ? __ldg(mean + col + 1) : 0.0;
 #pragma unroll
-        for (int i = 0; i < 4; i++) {
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-                const long long row = m0 + 64 * wm + 16 * i + g + 8 * h;
-                if (row >= n) continue;
-                const double x0 = mu0 + acc[i][j][2 * h], x1 = mu1 + acc[i][j][2 * h + 1];
-                if constexpr (LAYOUT == 0) {
-                    double *p = X + row * d + col;
-                    if (V == 2 && two) {
-                        *(double2 *)p = make_double2(x0, x1);
-                    } else {
-                        p[0] = x0;
-                        if (two) p[1] = x1;
-                    }
+        for (int i = 0; i < 8; i++) {
+            const long long row = m0 + 64 * wm + 8 * i + g;
+            if (row >= n) continue;
+            const double x0 = mu0 + acc[i][j][0], x1 = mu1 + acc[i][j][1];
+            if constexpr (LAYOUT == 0) {
+                double *p = X + row * d + col;
+                if (V == 2 && two) {
+                    *(double2 *)p = make_double2(x0, x1);
                 } else {
-                    X[(long long)col * n + row] = x0;
-                    if (two) X[(long long)(col + 1) * n + row] = x1;
+                    p[0] = x0;
+                    if (two) p[1] = x1;
                 }
+            } else {
+                X[(long long)col * n + row] = x0;
+                if (two) X[(long long)(col + 1) * n + row] = x1;
             }
         }
     }

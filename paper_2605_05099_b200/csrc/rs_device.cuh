@@ -1189,21 +1189,31 @@ struct DistU32 {  // bounded_uint(rng, b, 8|16|32) on halves (+ m: bounded_int i
 };
 
 // ----------------------------------------------------------------------------- run writers
-// Writes a contiguous run of 8-byte elements starting at element `start` of
-// `out`. VecWriter8 emits full 32-byte-aligned groups as one STG.256 (used where
-// registers are cheap); VecWriter2 emits 16-byte pairs (STG.128) with two slots,
-// for the register-bound parse kernels. Ragged heads/tails are scalar stores.
+// Writes a contiguous run of elements starting at element `start` of `out`, in 32-byte
+// groups (one STG.256 each); ragged heads/tails (shared with the neighbouring runs) are
+// element stores.
+//
+// Every writer keeps its own per-thread pointer to the current group and advances it,
+// never a (uniform base + per-thread index) pair recomputed at the store. Round 1 hit an
+// illegal-address fault in k_streams with the ring writer (x256** normals, 64 streams x
+// 4096): cuda-gdb put the faulting PC on the flush STG.256, whose address ptxas had built
+// as uniform register UR6:UR7 (the 32-byte-aligned output base) + the thread's group
+// index, with UR7 reloaded inside the divergent flush branch. The same loop also wrote
+// UR7 (shared-memory table base, sampler kind) on the sampler's divergent retry path, and
+// at the fault the warp's lanes were spread over the sampler and the flush. Uniform
+// registers are one per warp, so a divergent group running the sampler between the
+// flush group's reload and its store replaced the address's high word (DESIGN 7,
+// profiles/r02_ringwriter/). A per-thread pointer carried across iterations lives in
+// vector registers, which divergent groups do not share.
 template <class T>
 struct VecWriter8 {
-    T *abase;      // 32-byte aligned base
-    u64 vi;        // element index (from abase) of the current group
+    T *gp;         // this thread's current 32-byte group
     int slot, first;
     T v0, v1, v2, v3;
     RS_DEV void init(T *out, u64 start) {
         uintptr_t a = (uintptr_t)out;
-        abase = (T *)(a & ~(uintptr_t)31);
         u64 s = start + ((a & 31) >> 3);
-        vi = s & ~3ULL;
+        gp = (T *)(a & ~(uintptr_t)31) + (s & ~3ULL);
         slot = (int)(s & 3);
         first = slot;
     }
@@ -1217,7 +1227,7 @@ struct VecWriter8 {
         if (++slot == 4) flush_full();
     }
     RS_DEV void flush_full() {
-        T *p = abase + vi;
+        T *p = gp;
         if (first == 0) {
             u64 a = *(u64 *)&v0, b = *(u64 *)&v1, c = *(u64 *)&v2, d = *(u64 *)&v3;
             asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d)
@@ -1229,43 +1239,41 @@ struct VecWriter8 {
         }
         first = 0;
         slot = 0;
-        vi += 4;
+        gp += 4;
     }
     RS_DEV void finish() {
-        T *p = abase + vi;
+        T *p = gp;
         if (first == 0 && slot > 0) p[0] = v0;
         if (first <= 1 && slot > 1) p[1] = v1;
         if (first <= 2 && slot > 2) p[2] = v2;
     }
 };
 
-// Writes one thread's contiguous output run [start, ...) in 32-byte groups: the
-// current group is staged in a per-thread shared-memory ring (slot-major, so a warp's
-// STS is conflict-free) and leaves as one STG.256 once full. Partial head/tail groups
-// (shared with the neighbouring runs) are written element by element. Unlike a
-// register array with a dynamic slot index, put() is branch-free apart from the flush.
+// The current group is staged in a per-thread shared-memory ring (slot-major with stride
+// NT = the launch's block size, so a warp's STS is conflict-free) and leaves as one
+// STG.256 once full. Unlike a register array with a dynamic slot index, put() is
+// branch-free apart from the flush.
 template <class T, int NT>
 struct RingWriter {
     static constexpr int G = 32 / (int)sizeof(T);
-    T *abase;  // 32-byte aligned base
-    u64 vi;    // element index (from abase) of the current group
+    T *gp;     // this thread's current 32-byte group
     int slot, first;
     T *ring;   // this thread's slot 0; slot k at ring[k * NT]
     RS_DEV void init(T *out, u64 start, T *ring_) {
         ring = ring_;
         uintptr_t a = (uintptr_t)out;
-        abase = (T *)(a & ~(uintptr_t)31);
         u64 s = start + (u64)((a & 31) / sizeof(T));
-        vi = s & ~(u64)(G - 1);
+        gp = (T *)(a & ~(uintptr_t)31) + (s & ~(u64)(G - 1));
         slot = (int)(s & (G - 1));
         first = slot;
     }
+    RS_DEV T *at() const { return gp + slot; }  // where the next element goes
     RS_DEV void put(T v) {
         ring[slot * NT] = v;
         if (++slot == G) flush_full();
     }
     RS_DEV void flush_full() {
-        T *p = abase + vi;
+        T *p = gp;
         if (first == 0) {
             u64 q[4];
 #pragma unroll
@@ -1284,10 +1292,10 @@ struct RingWriter {
         }
         first = 0;
         slot = 0;
-        vi += G;
+        gp += G;
     }
     RS_DEV void finish() {
-        T *p = abase + vi;
+        T *p = gp;
         for (int k = first; k < slot; k++) p[k] = ring[k * NT];
     }
 };
@@ -1301,26 +1309,28 @@ struct RingWriter {
 template <class T, int NT, int GB = 32>  // GB: bytes per group (32: one STG.256)
 struct BatchRing {
     static constexpr int G = GB / (int)sizeof(T);
-    T *abase;  // 32-byte aligned base
-    u64 pos;   // element index (from abase) of the next sample
-    u64 fl;    // first element not yet stored
-    T *ring;   // this thread's slot 0; slot k at ring[k * NT]
+    T *gp;        // this thread's current (unstored) group, 32-byte aligned
+    u32 head;     // elements of that group before the run (shared with the previous run)
+    u32 npend;    // elements from the group start up to the next sample (head included)
+    u32 rbase;    // ring slot of the group's first element (0 or G)
+    T *ring;      // this thread's slot 0; slot k at ring[k * NT]
     RS_DEV void init(T *out, u64 start, T *ring_) {
         ring = ring_;
         uintptr_t a = (uintptr_t)out;
-        abase = (T *)(a & ~(uintptr_t)31);
-        pos = fl = start + (u64)((a & 31) / sizeof(T));
+        const u64 s = start + (u64)((a & 31) / sizeof(T));
+        gp = (T *)(a & ~(uintptr_t)31) + (s & ~(u64)(G - 1));
+        head = npend = (u32)(s & (G - 1));
+        rbase = (u32)(s & (2 * G - 1)) & ~(u32)(G - 1);
     }
     RS_DEV void put(T v) {
-        ring[(int)(pos & (2 * G - 1)) * NT] = v;
-        pos++;
+        ring[(int)((rbase + npend) & (2 * G - 1)) * NT] = v;
+        npend++;
     }
     RS_DEV void tick() {
-        u64 g0 = fl & ~(u64)(G - 1);
-        if (pos < g0 + G) return;
-        T *p = abase + g0;
-        int b = (int)(g0 & (2 * G - 1));  // ring slot of the group's first element
-        if (fl == g0) {
+        if (npend < (u32)G) return;
+        T *p = gp;
+        const int b = (int)rbase;
+        if (head == 0) {
             constexpr int E32 = 32 / (int)sizeof(T);  // elements per 32-byte store
 #pragma unroll
             for (int h = 0; h < GB / 32; h++) {
@@ -1339,12 +1349,15 @@ struct BatchRing {
                              "l"(q[2]), "l"(q[3]) : "memory");
             }
         } else {  // the run's first group is shared with the previous run
-            for (int k = (int)(fl - g0); k < G; k++) p[k] = ring[(b + k) * NT];
+            for (int k = (int)head; k < G; k++) p[k] = ring[(b + k) * NT];
         }
-        fl = g0 + G;
+        gp += G;
+        npend -= G;
+        rbase ^= G;
+        head = 0;
     }
     RS_DEV void finish() {
-        for (u64 a = fl; a < pos; a++) abase[a] = ring[(int)(a & (2 * G - 1)) * NT];
+        for (u32 k = head; k < npend; k++) gp[k] = ring[(int)((rbase + k) & (2 * G - 1)) * NT];
     }
 };
 

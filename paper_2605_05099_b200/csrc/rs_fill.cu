@@ -68,6 +68,14 @@ struct DevCtx {
     size_t spec_bytes = 0;
     void *pre = nullptr;
     size_t pre_bytes = 0;
+    // single-pass tile parse (k_tile.cu): tile status + control words + pcg64 tile states,
+    // the pcg64 lane table A^(TL_W l) for the increment `lane_inc`, and a pinned upload area
+    void *tile_buf = nullptr;
+    size_t tile_bytes = 0;
+    u64 *pcg_lane = nullptr;
+    u64 lane_inc[2] = {0, 0};
+    bool have_lane = false;
+    u64 *up_dev = nullptr, *up_host = nullptr;
     // the counted slice of rs_range_count, waiting for rs_range_emit (its plan refers to
     // the scratch above, so any other fill on this device invalidates it)
     struct Range {
@@ -120,6 +128,8 @@ rs_status init_dev(int dev, DevCtx **out) {
     CK(cudaMalloc(&c.overrun, sizeof(u32)));
     CK(cudaMemset(c.overrun, 0, sizeof(u32)));
     CK(cudaMallocHost(&c.res_host, sizeof(DevResult)));
+    CK(cudaMalloc(&c.up_dev, 256 * 8));
+    CK(cudaMallocHost(&c.up_host, 256 * 8));
     c.ready = true;
     return RS_OK;
 }
@@ -717,6 +727,151 @@ rs_status prep_chunk(DevCtx &c, FillPlan &p, const Resolved &r, bool mem, cudaSt
     return RS_OK;
 }
 
+// Warp-tile parse (k_tile.cu) for Philox / PCG64 and the one-word-token laws (word-level
+// normal and exponential kinds, Lemire): count -> two table scans -> emit, every warp-tile
+// independent. RS_ERR_UNSUPPORTED: not applicable, or a rare case the tables do not cover
+// (the caller takes the two-pass path). Synchronous; E = logical words consumed.
+rs_status run_tile(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void *dout, cudaStream_t st, u64 &E,
+                   u64 *tal) {
+    const int e = s->engine;
+    if (!getenv("RS_TILE")) return RS_ERR_UNSUPPORTED;  // opt-in: measured slower than the two-pass path (DESIGN 4.6)
+    if ((e != RS_ENG_PCG64 && e != RS_ENG_PHILOX) || r.unit != 1) return RS_ERR_UNSUPPORTED;
+    const int fam = r.family;
+    if (!(fam == FAM_NORM && r.kind != NK_SKEW) && fam != FAM_EXP && fam != FAM_LEMIRE) return RS_ERR_UNSUPPORTED;
+    // The logical stream is the buffered words then the engine. The buffer holds the
+    // engine's last refill (buffer.py:29-35), so rewinding the engine over that refill
+    // makes the whole stream engine words: raw word `skip` = the stream's first word.
+    u64 base[32];
+    memcpy(base, s->state, sizeof base);
+    u64 skip = 0;
+    const int P = s->fill - s->cursor;
+    if (P > 0) {
+        if (s->fill != CAP) return RS_ERR_UNSUPPORTED;
+        if (e == RS_ENG_PCG64) {
+            rs::pcg_advance(base, (u128)0 - (u128)CAP);  // period 2^128: A^(-144)
+        } else {  // counter - 36 blocks (256-bit borrow)
+            u64 b = CAP / 4;
+            for (int i = 0; i < 4; i++) {
+                const u64 o = base[i];
+                base[i] = o - b;
+                b = o < b ? 1 : 0;
+            }
+        }
+        u64 chk[32], w[CAP];
+        memcpy(chk, base, sizeof chk);
+        rs::engine_generate(e, chk, w, CAP);
+        if (memcmp(w, s->buf, sizeof w) != 0) return RS_ERR_UNSUPPORTED;  // not a refill of this engine
+        skip = (u64)s->cursor;
+    }
+    if (!rsk::tile_kernels(e, fam, 0).count) return RS_ERR_UNSUPPORTED;
+    const double ww = (double)n * r.words_per_sample;
+    const u64 words = skip + (u64)(ww * 1.01 + 16.0 * std::sqrt(ww) + 4096.0);
+    const u64 nwt = (words + WT_WORDS - 1) / WT_WORDS;
+    const u64 nblk = (nwt + WT_BLK - 1) / WT_BLK;
+    if (nblk > 0xFFFFFFFFULL) return RS_ERR_UNSUPPORTED;
+    int fold = 0;
+    if (e == RS_ENG_PHILOX) {
+        const u64 blocks = nwt * (WT_WORDS / 4);
+        fold = base[0] + blocks >= base[0] ? 1 : 0;  // counter word 0 never carries in the fill
+    }
+    const rsk::TileLaunch tl = rsk::tile_kernels(e, fam, fold);
+    // scratch: tables [nwt] 32 B, prefixes [nwt] 48 B, block tables / entries, ctl, pcg64 states
+    const size_t o_pre = nwt * sizeof(WTTab), o_blk = o_pre + nwt * sizeof(WTTab32);
+    const size_t o_in = o_blk + nblk * sizeof(WTTab32), o_ctl = o_in + nblk * 16, o_pcg = o_ctl + 64;
+    const size_t need = o_pcg + (e == RS_ENG_PCG64 ? nwt * 16 : 0);
+    if (need > c.tile_bytes) {
+        cudaFree(c.tile_buf);
+        c.tile_buf = nullptr;
+        c.tile_bytes = 0;
+        CK(cudaMalloc(&c.tile_buf, need));
+        c.tile_bytes = need;
+    }
+    char *tb = (char *)c.tile_buf;
+    WTPlan p;
+    memset(&p, 0, sizeof p);
+    p.engine = e;
+    p.kind = r.kind;
+    p.fm = s->full_mantissa;
+    p.n = n;
+    p.skip = skip;
+    p.nwt = nwt;
+    for (int i = 0; i < 6; i++) p.base[i] = base[i];
+    memcpy(p.fp, r.fp, sizeof p.fp);
+    memcpy(p.ip, r.ip, sizeof p.ip);
+    p.zslow = (r.table == 0 || r.table == 1) ? c.zslow[r.table] : nullptr;
+    p.zfast = (r.table == 0 || r.table == 1) ? c.zfast[r.table] : nullptr;
+    p.out = dout;
+    p.tab = (WTTab *)tb;
+    p.pre = (WTTab32 *)(tb + o_pre);
+    p.blk = (WTTab32 *)(tb + o_blk);
+    p.blk_in = (u64 *)(tb + o_in);
+    p.nblk = (u32)nblk;
+    p.ctl = (u32 *)(tb + o_ctl);
+    p.res = c.res;
+    CK(cudaMemsetAsync(p.ctl, 0, 64, st));
+    CK(cudaMemsetAsync(c.res, 0, offsetof(DevResult, serial_state), st));
+    rs_status rc;
+    if (e == RS_ENG_PHILOX) {
+        for (int i = 0; i < 10; i++) {  // round keys k + r W (counter.py:95-96)
+            p.rk0[i] = base[4] + (u64)i * 0x9E3779B97F4A7C15ULL;
+            p.rk1[i] = base[5] + (u64)i * 0xBB67AE8584CAA73BULL;
+        }
+    } else {
+        const u128 inc = ((u128)base[3] << 64) | base[2];
+        if (!c.have_lane || c.lane_inc[0] != base[2] || c.lane_inc[1] != base[3]) {
+            u64 lt[4 * 32];
+            for (int l = 0; l < 32; l++) {  // A^(WT_W l), pcg.py:41-55
+                u128 m, a;
+                rs::pcg_affine(inc, (u128)WT_W * l, m, a);
+                lt[4 * l] = (u64)m; lt[4 * l + 1] = (u64)(m >> 64);
+                lt[4 * l + 2] = (u64)a; lt[4 * l + 3] = (u64)(a >> 64);
+            }
+            if (!c.pcg_lane) CK(cudaMalloc(&c.pcg_lane, sizeof lt));
+            CK(cudaMemcpy(c.pcg_lane, lt, sizeof lt, cudaMemcpyHostToDevice));
+            c.lane_inc[0] = base[2];
+            c.lane_inc[1] = base[3];
+            c.have_lane = true;
+        }
+        // base state + A^(WT_WORDS 2^j), j < 40, for the warp-tile states
+        u64 *up = c.up_host;
+        for (int i = 0; i < 4; i++) up[i] = base[i];
+        for (int j = 0; j < 40; j++) {
+            u128 m, a;
+            rs::pcg_affine(inc, (u128)WT_WORDS << j, m, a);
+            up[4 + 4 * j] = (u64)m; up[5 + 4 * j] = (u64)(m >> 64);
+            up[6 + 4 * j] = (u64)a; up[7 + 4 * j] = (u64)(a >> 64);
+        }
+        CK(cudaMemcpyAsync(c.up_dev, up, (4 + 160) * 8, cudaMemcpyHostToDevice, st));
+        u64 *states = (u64 *)(tb + o_pcg);
+        const u64 *bp = c.up_dev, *pw = c.up_dev + 4;
+        u64 nn = nwt;
+        void *ka[] = {&bp, &pw, &states, &nn};
+        if ((rc = launch(rsk::pcg_wt_kernel(), dim3((unsigned)((nwt + 255) / 256)), dim3(256), ka, st))) return rc;
+        p.pcg_lane = c.pcg_lane;
+        p.pcg_wt = states;
+    }
+    void *args[] = {&p};
+    const u64 gc = (u64)c.sms * (u64)occupancy(tl.count);
+    if ((rc = launch(tl.count, dim3((unsigned)std::min<u64>(gc, (nwt + 7) / 8)), dim3(256), args, st))) return rc;
+    const size_t scan_smem = 2 * WT_BLK * 40;
+    CK(cudaFuncSetAttribute(rsk::wt_scan1_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem));
+    CK(cudaFuncSetAttribute(rsk::wt_scan2_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem));
+    if ((rc = launch(rsk::wt_scan1_kernel(), dim3((unsigned)nblk), dim3(WT_BLK), args, st, scan_smem))) return rc;
+    if ((rc = launch(rsk::wt_scan2_kernel(), dim3(1), dim3(WT_BLK), args, st, scan_smem))) return rc;
+    const u64 ge = (u64)c.sms * (u64)occupancy(tl.emit, tl.emit_smem);
+    if ((rc = launch(tl.emit, dim3((unsigned)std::min<u64>(ge, (nwt + 7) / 8)), dim3(256), args, st, tl.emit_smem)))
+        return rc;
+    CK(cudaMemcpyAsync(c.res_host, c.res, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+    u32 *ctl_host = (u32 *)(c.up_host + 200);
+    CK(cudaMemcpyAsync(ctl_host, p.ctl, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const u64 total = ((u64)ctl_host[3] << 32) | ctl_host[2];
+    if (ctl_host[0] || ctl_host[1] || total < n) return RS_ERR_UNSUPPORTED;  // the two-pass path redoes it
+    E = c.res_host->end_pos - skip;
+    for (int i = 0; i < 6; i++) tal[i] = c.res_host->tally[i];
+    return RS_OK;
+}
+
 // The device part of one fill. On return (sync=true) `E` holds the stream units
 // consumed (64-bit words, or 32-bit halves incl. a used pending half when r.unit == 2)
 // and `tal` the tallies.
@@ -804,6 +959,14 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
         return RS_OK;
     }
 
+    if (sync) {  // the single-pass tile parse where it applies (counter / affine engines)
+        rc = run_tile(c, s, r, n, dout, st, E, tal);
+        if (rc != RS_ERR_UNSUPPORTED) {
+            chunks = 1;
+            return rc;
+        }
+        rs::clear_error();
+    }
     // variable consumption: chunks of provisioned words until n samples exist.
     // Chunk coordinates: chunk-local position lp in units; chunk 1 starts with the
     // pending half (u = 2) and the P buffered words, then the engine; a later chunk

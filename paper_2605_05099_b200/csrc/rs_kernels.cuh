@@ -89,6 +89,50 @@ struct FillPlan {
     u32 *c1own;                   // phase-1 samples before the merge (all of them if none)
     u32 *mrank0;                  // phase-0 sample index at the merge point
 };
+// ----------------------------------------------------------------------------- warp-tile parse
+// (k_tile.cu) Counter / affine engines (Philox, PCG64) reach any word directly, so the
+// stream is cut into warp-tiles of 512 consecutive words (32 lanes x 16), each parsed by
+// one warp with no dependence on any other: a count pass tabulates each warp-tile's
+// (exit, count) for entries 0..7, two small scans compose the tables, and the emit pass
+// parses each warp-tile from its exact entry and writes its samples with a bulk copy.
+struct DevResult;
+constexpr int WT_W = 16;                       // words per lane window
+constexpr u64 WT_WORDS = 32 * WT_W;            // words per warp-tile
+constexpr int WT_D = 8;                        // tabulated entries 0..WT_D-1
+constexpr int WT_BLK = 1024;                   // warp-tiles per scan block
+struct WTTab {                                 // a warp-tile's table (K1), 32 B
+    u32 x[2];                                  // exits (bytes) for entries 0..7; 0xFF: undefined
+    u32 c[4];                                  // counts (u16 pairs)
+    u32 pad[2];
+};
+struct WTTab32 {                               // composed tables (scans), 48 B
+    u32 x[2];
+    u32 c[WT_D];
+    u32 pad[2];
+};
+struct WTPlan {
+    int engine, kind, fm, pad;
+    u64 n;                                     // samples
+    u64 skip;                                  // raw word where the logical stream (sample 0) starts
+    u64 nwt;                                   // warp-tiles
+    u64 base[6];                               // rewound engine: pcg64 slo, shi, ilo, ihi; philox c0-c3, k0, k1
+    u64 rk0[10], rk1[10];                      // philox round keys
+    const u64 *pcg_lane;                       // [32][4]: A^(WT_W l) as (mul lo, hi, add lo, hi)
+    const u64 *pcg_wt;                         // [nwt][2]: the state at raw word WT_WORDS w
+    double fp[4];
+    u64 ip[4];
+    const RsZigSlow *zslow;
+    const ZigFast *zfast;
+    void *out;
+    WTTab *tab;                                // [nwt]
+    WTTab32 *pre;                              // [nwt] exclusive in-block prefix tables
+    WTTab32 *blk;                              // [nblk] block tables
+    u64 *blk_in;                               // [nblk][2] exact (entry, offset) entering each block
+    u32 nblk;
+    u32 *ctl;                                  // [0] undefined entry, [1] parse mismatch; [2..3] total (u64)
+    DevResult *res;
+};
+
 // per-sample tally word of the gamma attempt machine: gamma attempts (8 bits), normal
 // attempts (12), normal pdf evaluations (12); 0xFFFFFFFF never occurs (flagged instead)
 __device__ __forceinline__ bool pack_tally(u32 ga, u32 na, u32 np, u32 &w) {
@@ -1561,8 +1605,10 @@ __device__ __forceinline__ void stream_rows8(u64 *out, u64 j, u64 nper, bool val
     const u64 row = (u64)(uintptr_t)(out + j * nper);
     for (u64 k = 0; k < nch; k++) {
         if (valid) {
+            // a per-lane pointer bound, not a uniform counter (see k_streams' row loop)
+            u64 *q = tile + fx_at(lane, 0), *const qe = q + FX_CH;
 #pragma unroll 4
-            for (int c = 0; c < FX_CH; c++) tile[fx_at(lane, c)] = produce();
+            while (q < qe) *q++ = produce();
         }
         __syncwarp();
         const u64 dst = valid ? row + k * FX_CH * 8 : 0;
@@ -1708,18 +1754,18 @@ __global__ void __launch_bounds__(STR_BLOCK) k_streams(const __grid_constant__ S
         e.s0 = w[0]; e.s1 = w[1]; e.s2 = w[2]; e.s3 = w[3];
     }
     }  // valid
-    // Per-stream rows go out through VecWriter8 (8-byte) / ScalarWriter (4-byte). The
-    // shared-memory RingWriter used by k_emit produced an illegal address here in some
-    // configurations (x256**/pcg64 normals, >= 8 streams) that vanished under printf
-    // instrumentation; it stays out of this kernel until that is understood.
+    // Rows that cannot take the warp tile go out through the shared-memory RingWriter (one
+    // STG.256 per 32-byte group). Its round-1 fault here was a uniform-register hazard in
+    // the writer's address arithmetic under divergence, not the ring (rs_device.cuh run
+    // writers, DESIGN 7); the writers now carry per-thread group pointers.
     if constexpr (D == FAM_FIXED) {  // raw / uniform / masked laws: a fresh stream, no pending half
         if (tiled) {
             stream_rows8((u64 *)a.out, j, a.nper, valid, tile, [&]() { return fx_map_rt(a, e.next()); });
             return;
         }
         if (is_half(a.fmode)) {  // low half first, a trailing high half dropped
-            ScalarWriter<u32> wr;
-            wr.init((u32 *)a.out, j * a.nper);
+            RingWriter<u32, STR_BLOCK> wr;
+            wr.init((u32 *)a.out, j * a.nper, (u32 *)st_dyn + threadIdx.x);
             for (u64 i = 0; i < a.nper; i += 2) {
                 u64 q = fx_map_rt(a, e.next());
                 wr.put((u32)q);
@@ -1727,8 +1773,8 @@ __global__ void __launch_bounds__(STR_BLOCK) k_streams(const __grid_constant__ S
             }
             wr.finish();
         } else {
-            VecWriter8<u64> wr;
-            wr.init((u64 *)a.out, j * a.nper);
+            RingWriter<u64, STR_BLOCK> wr;
+            wr.init((u64 *)a.out, j * a.nper, st_dyn + threadIdx.x);
             for (u64 i = 0; i < a.nper; i++) wr.put(fx_map_rt(a, e.next()));
             wr.finish();
         }
@@ -1759,8 +1805,8 @@ __global__ void __launch_bounds__(STR_BLOCK) k_streams(const __grid_constant__ S
             return;
         }
     }
-    typename std::conditional<sizeof(T) == 8, VecWriter8<T>, ScalarWriter<T>>::type wr;
-    wr.init((T *)a.out, j * a.nper);
+    RingWriter<T, STR_BLOCK> wr;
+    wr.init((T *)a.out, j * a.nper, (T *)st_dyn + threadIdx.x);
     if constexpr (D == FAM_LEMIRE) {
         for (u64 i = 0; i < a.nper;) {
             u64 o;
@@ -1772,11 +1818,19 @@ __global__ void __launch_bounds__(STR_BLOCK) k_streams(const __grid_constant__ S
             u32 o;
             if (d.accept(h.next32(), o)) { wr.put(o); i++; }
         }
-    } else if constexpr (DT::HALF) {
-        EngHalves<typename EngOf<E>::type> h{&e, 0, false};
-        for (u64 i = 0; i < a.nper; i++) wr.put(d.sample(h, tl));
     } else {
-        for (u64 i = 0; i < a.nper; i++) wr.put(d.sample(e, tl));
+        // The loop runs to this row's end pointer, not to a sample counter: every lane has the
+        // same trip count nper, so ptxas kept such a counter in a uniform register, and it
+        // merged the sampler's rejection retry into this loop's back edge -- the lanes that
+        // produced a sample advanced the one warp-wide counter for the lanes that had
+        // rejected (rows ended short; DESIGN 7). A per-lane bound cannot be uniform.
+        T *const rend = (T *)a.out + (j + 1) * a.nper;
+        if constexpr (DT::HALF) {
+            EngHalves<typename EngOf<E>::type> h{&e, 0, false};
+            while (wr.at() < rend) wr.put(d.sample(h, tl));
+        } else {
+            while (wr.at() < rend) wr.put(d.sample(e, tl));
+        }
     }
     wr.finish();
 }
@@ -1800,6 +1854,14 @@ const void *streams_kernel(int engine, int fam); // k_streams_a.cu (dispatch), k
 const void *streams_kernel_b(int engine, int fam);
 const void *serial_kernel(int engine, int fam, int fixed_mode);  // k_misc.cu
 const void *setup_kernel();     // k_misc.cu: k_x256_setup
+struct TileLaunch {  // k_tile.cu: warp-tile parse for philox / pcg64 (norm, exp, Lemire)
+    const void *count, *emit;
+    size_t emit_smem;
+};
+TileLaunch tile_kernels(int engine, int fam, int fold);  // count == nullptr: not covered
+const void *pcg_wt_kernel();   // per-warp-tile pcg64 states
+const void *wt_scan1_kernel(); // in-block scans of the tables
+const void *wt_scan2_kernel(); // block chain
 struct MvnLaunch {  // k_mvn.cu: the FP64 tensor-core contraction X = mean + z L^T
     const void *fn;
     size_t smem;

@@ -261,6 +261,25 @@ def test_streams_tiled_rows(engine):
             assert np.array_equal(_bits(host[j]), _bits(o.fill(dist, params, n))), (dist, j)
 
 
+@pytest.mark.parametrize("engine", ["x256**", "pcg64", "sfc64"])
+def test_streams_ring_writer_rows(engine):
+    """Rows that cannot take the warp tile (odd row length, 4-byte laws) leave through the
+    shared-memory RingWriter. Its round-1 fault configuration -- x256** normals, 64 streams
+    x 4096 -- and the same shapes at odd lengths, every row checked (DESIGN 7)."""
+    for dist, params, ns, n in (("norm", {}, 64, 4097), ("norm", {}, 64, 777), ("exp", {}, 256, 4097),
+                                ("gamma", {"alpha": 2.5}, 64, 1025), ("normf", {}, 64, 4096),
+                                ("uint32", {"b": 7}, 96, 2049), ("u01f", {}, 70, 1001)):
+        host = _np(fill_streams(engine, [5], [2], 10, ns, dist, params, n))
+        rngs = [O.OracleRng(engine, seed=[5], spawn_key=(2, 10 + j)) for j in range(ns)]
+        refs = O.threaded_fill(rngs, dist, params, n)
+        for j in range(ns):
+            assert np.array_equal(_bits(host[j]), _bits(refs[j])), (dist, ns, n, j)
+    # the round-1 fault configuration itself (tiled rows now; 4096 is even)
+    host = _np(fill_streams(engine, [5], [2], 10, 64, "norm", {}, 4096))
+    o = O.OracleRng(engine, seed=[5], spawn_key=(2, 10 + 63))
+    assert np.array_equal(_bits(host[63]), _bits(o.fill("norm", {}, 4096)))
+
+
 def test_streams_continuous():
     out = _np(fill_streams("sfc64", [5], [2], 10, 300, "norm", {}, 777))
     for j in (0, 299):

@@ -1,4 +1,5 @@
-"""Run one BASELINE fill config a few times through rs_fill_async (for ncu / timing).
+"""Run one BASELINE fill config a few times through rs_fill, the product call (for ncu /
+timing; each rep restarts from the same stream position).
 
     python tools/profile_fill.py ENGINE DIST LOG2N [key=value ...] [--reps R] [--fm]
 e.g. python tools/profile_fill.py philox u01 30 --fm
@@ -39,10 +40,13 @@ el = 4 if a.dist in ("u01f", "uniff", "normf", "expf") else 8
 out = torch.empty(n * el, dtype=torch.uint8, device="cuda")
 sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(a.reps + 1)]
+res = _lib.RsFillResult()
 for i in range(a.reps):
+    s2 = _lib.RsStream()
+    ctypes.memmove(ctypes.byref(s2), ctypes.byref(s), ctypes.sizeof(s))
     ev[i].record()
-    _lib.check(_lib.lib.rs_fill_async(ctypes.byref(s), _lib.DIST_IDS[a.dist], fpa, ipa, n,
-                                      ctypes.c_void_p(out.data_ptr()), sp))
+    _lib.check(_lib.lib.rs_fill(ctypes.byref(s2), _lib.DIST_IDS[a.dist], fpa, ipa, n,
+                                ctypes.c_void_p(out.data_ptr()), ctypes.byref(res), sp))
 ev[a.reps].record()
 torch.cuda.synchronize()
 ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(a.reps)]

@@ -64,6 +64,9 @@ def run(d, n, dense=False, layout=0, reps=5):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # e.g. `512`: one C5a shape (for ncu)
+        run(int(sys.argv[1]), 1 << 20, reps=1)
+        sys.exit(0)
     for d in (64, 256, 512):
         run(d, 1 << 20)
     run(512, 1 << 20, layout=1)
