@@ -580,6 +580,50 @@ rs_status get_out(DevCtx &c, void *out, size_t bytes, Staging &sg) {
     return RS_OK;
 }
 
+// The 2-D tensor map of k_fixed's TMA stores: R rows of L 8-byte words (row r = segment r),
+// 32 x 16-word boxes in the 128-byte swizzle. cuTensorMapEncodeTiled comes from the driver
+// through the runtime's entry-point query (no link against libcuda).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+bool make_row_tmap(CUtensorMap *tm, void *base, u64 L, u64 R) {
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)f;
+        cudaGetLastError();
+    }
+    if (!fn || (((uintptr_t)base) & 15) || R < 32 || L < 16 || (L * 8) % 16 || R > 0xFFFFFFFFULL || L > 0xFFFFFFFFULL)
+        return false;
+    const cuuint64_t dims[2] = {L, R}, strides[1] = {L * 8};
+    const cuuint32_t box[2] = {16, 32}, es[2] = {1, 1};
+    return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// k_fixed launch: TMA row stores when the output allows it (the full segments form a 2-D tensor)
+rs_status launch_fixed(DevCtx &c, FillPlan &p, const void *fn, u64 wfull, cudaStream_t st) {
+    CUtensorMap tm;
+    memset(&tm, 0, sizeof tm);
+    p.tma = 0;
+    p.tma_rows = 0;
+    static const int tma_mode = getenv("RS_TMA") ? atoi(getenv("RS_TMA")) : 0;
+    if (tma_mode && !p.pending_used && wfull > (u64)p.P) {
+        const u64 R = (wfull - (u64)p.P) / p.L;
+        if (make_row_tmap(&tm, (u64 *)p.out + p.P, p.L, R)) {
+            p.tma = tma_mode;
+            p.tma_rows = R;
+        }
+    }
+    void *args[] = {&p, &tm};
+    return launch(fn, dim3(p.T / BLOCK), dim3(BLOCK), args, st, FX_SMEM);
+}
+
 // interleaved xoshiro fixed fill: lane states jumped per step group on the device
 rs_status launch_simd(DevCtx &c, FillPlan &p, int mode, cudaStream_t st) {
     const void *fn = simd_kernel(p.engine, mode);
@@ -630,8 +674,7 @@ rs_status launch_raw_words(DevCtx &c, FillPlan &m, cudaStream_t st) {
     }
     const void *fn = fixed_kernel(m.engine, FX_RAW);
     if ((rc = plan_segments(c, m, m.weng, 64, occupancy(fn, FX_SMEM), st, true, 144))) return rc;
-    void *args[] = {&m};
-    return launch(fn, dim3(m.T / BLOCK), dim3(BLOCK), args, st, FX_SMEM);
+    return launch_fixed(c, m, fn, m.weng, st);
 }
 
 // shortest segment of a variable-consumption plan (gamma-family resync distances)
@@ -951,9 +994,10 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
         const void *fn = fixed_kernel(s->engine, r.fixed_mode);
         rc = plan_segments(c, p, p.weng ? p.weng : 1, 64, occupancy(fn, FX_SMEM), st, true, 144);
         if (rc) return rc;
-        void *args[] = {&p};
-        rc = launch(fn, dim3(p.T / BLOCK), dim3(BLOCK), args, st, FX_SMEM);
-        if (rc) return rc;
+        // logical words whose output is complete (half modes: both halves; a trailing low
+        // half and the pending half stay on the element-store path)
+        const u64 wfull = u == 2 ? (p.pending_used ? 0 : n / 2) : n;
+        if ((rc = launch_fixed(c, p, fn, wfull, st))) return rc;
         E = n;
         chunks = 1;
         return RS_OK;
@@ -1298,7 +1342,14 @@ rs_status rs_fill_streams(int32_t engine, const uint64_t *seed, int32_t n_seed, 
     // smaller tile keeps 2^16 streams in one wave
     if (d == FAM_LEMIRE && a.ip[1] > (1ULL << 60)) d = FAM_LEMIRE_RING;
     const void *fn = rsk::streams_kernel(engine, d);
-    void *args[] = {&a};
+    // 8-byte rows as a 2-D tensor (row = stream) for the TMA store path
+    CUtensorMap tm;
+    memset(&tm, 0, sizeof tm);
+    a.tma = 0;
+    if (getenv("RS_TMA") && elem_size(dist) == 8 && n_per_stream % 2 == 0 && d != FAM_LEMIRE_RING &&
+        !(d == FAM_FIXED && (r.fixed_mode == FX_U01F || r.fixed_mode == FX_HMAP)))
+        a.tma = make_row_tmap(&tm, sg.dptr, n_per_stream, n_streams) ? 1 : 0;
+    void *args[] = {&a, &tm};
     unsigned g2 = (unsigned)((n_streams + STR_BLOCK - 1) / STR_BLOCK);
     if ((rc = launch(fn, dim3(g2), dim3(STR_BLOCK), args, st, d == FAM_LEMIRE_RING ? ST_SMEM_RING : ST_SMEM)))
         return rc;
