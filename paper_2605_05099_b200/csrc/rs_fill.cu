@@ -68,14 +68,6 @@ struct DevCtx {
     size_t spec_bytes = 0;
     void *pre = nullptr;
     size_t pre_bytes = 0;
-    // single-pass tile parse (k_tile.cu): tile status + control words + pcg64 tile states,
-    // the pcg64 lane table A^(TL_W l) for the increment `lane_inc`, and a pinned upload area
-    void *tile_buf = nullptr;
-    size_t tile_bytes = 0;
-    u64 *pcg_lane = nullptr;
-    u64 lane_inc[2] = {0, 0};
-    bool have_lane = false;
-    u64 *up_dev = nullptr, *up_host = nullptr;
     // the counted slice of rs_range_count, waiting for rs_range_emit (its plan refers to
     // the scratch above, so any other fill on this device invalidates it)
     struct Range {
@@ -128,8 +120,6 @@ rs_status init_dev(int dev, DevCtx **out) {
     CK(cudaMalloc(&c.overrun, sizeof(u32)));
     CK(cudaMemset(c.overrun, 0, sizeof(u32)));
     CK(cudaMallocHost(&c.res_host, sizeof(DevResult)));
-    CK(cudaMalloc(&c.up_dev, 256 * 8));
-    CK(cudaMallocHost(&c.up_host, 256 * 8));
     c.ready = true;
     return RS_OK;
 }
@@ -580,47 +570,9 @@ rs_status get_out(DevCtx &c, void *out, size_t bytes, Staging &sg) {
     return RS_OK;
 }
 
-// The 2-D tensor map of k_fixed's TMA stores: R rows of L 8-byte words (row r = segment r),
-// 32 x 16-word boxes in the 128-byte swizzle. cuTensorMapEncodeTiled comes from the driver
-// through the runtime's entry-point query (no link against libcuda).
-typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-bool make_row_tmap(CUtensorMap *tm, void *base, u64 L, u64 R) {
-    static EncodeTiledFn fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
-        void *f = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = (EncodeTiledFn)f;
-        cudaGetLastError();
-    }
-    if (!fn || (((uintptr_t)base) & 15) || R < 32 || L < 16 || (L * 8) % 16 || R > 0xFFFFFFFFULL || L > 0xFFFFFFFFULL)
-        return false;
-    const cuuint64_t dims[2] = {L, R}, strides[1] = {L * 8};
-    const cuuint32_t box[2] = {16, 32}, es[2] = {1, 1};
-    return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-// k_fixed launch: TMA row stores when the output allows it (the full segments form a 2-D tensor)
-rs_status launch_fixed(DevCtx &c, FillPlan &p, const void *fn, u64 wfull, cudaStream_t st) {
-    CUtensorMap tm;
-    memset(&tm, 0, sizeof tm);
-    p.tma = 0;
-    p.tma_rows = 0;
-    static const int tma_mode = getenv("RS_TMA") ? atoi(getenv("RS_TMA")) : 0;
-    if (tma_mode && !p.pending_used && wfull > (u64)p.P) {
-        const u64 R = (wfull - (u64)p.P) / p.L;
-        if (make_row_tmap(&tm, (u64 *)p.out + p.P, p.L, R)) {
-            p.tma = tma_mode;
-            p.tma_rows = R;
-        }
-    }
-    void *args[] = {&p, &tm};
+// k_fixed launch
+rs_status launch_fixed(DevCtx &, FillPlan &p, const void *fn, cudaStream_t st) {
+    void *args[] = {&p};
     return launch(fn, dim3(p.T / BLOCK), dim3(BLOCK), args, st, FX_SMEM);
 }
 
@@ -674,7 +626,7 @@ rs_status launch_raw_words(DevCtx &c, FillPlan &m, cudaStream_t st) {
     }
     const void *fn = fixed_kernel(m.engine, FX_RAW);
     if ((rc = plan_segments(c, m, m.weng, 64, occupancy(fn, FX_SMEM), st, true, 144))) return rc;
-    return launch_fixed(c, m, fn, m.weng, st);
+    return launch_fixed(c, m, fn, st);
 }
 
 // shortest segment of a variable-consumption plan (gamma-family resync distances)
@@ -770,151 +722,6 @@ rs_status prep_chunk(DevCtx &c, FillPlan &p, const Resolved &r, bool mem, cudaSt
     return RS_OK;
 }
 
-// Warp-tile parse (k_tile.cu) for Philox / PCG64 and the one-word-token laws (word-level
-// normal and exponential kinds, Lemire): count -> two table scans -> emit, every warp-tile
-// independent. RS_ERR_UNSUPPORTED: not applicable, or a rare case the tables do not cover
-// (the caller takes the two-pass path). Synchronous; E = logical words consumed.
-rs_status run_tile(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void *dout, cudaStream_t st, u64 &E,
-                   u64 *tal) {
-    const int e = s->engine;
-    if (!getenv("RS_TILE")) return RS_ERR_UNSUPPORTED;  // opt-in: measured slower than the two-pass path (DESIGN 4.6)
-    if ((e != RS_ENG_PCG64 && e != RS_ENG_PHILOX) || r.unit != 1) return RS_ERR_UNSUPPORTED;
-    const int fam = r.family;
-    if (!(fam == FAM_NORM && r.kind != NK_SKEW) && fam != FAM_EXP && fam != FAM_LEMIRE) return RS_ERR_UNSUPPORTED;
-    // The logical stream is the buffered words then the engine. The buffer holds the
-    // engine's last refill (buffer.py:29-35), so rewinding the engine over that refill
-    // makes the whole stream engine words: raw word `skip` = the stream's first word.
-    u64 base[32];
-    memcpy(base, s->state, sizeof base);
-    u64 skip = 0;
-    const int P = s->fill - s->cursor;
-    if (P > 0) {
-        if (s->fill != CAP) return RS_ERR_UNSUPPORTED;
-        if (e == RS_ENG_PCG64) {
-            rs::pcg_advance(base, (u128)0 - (u128)CAP);  // period 2^128: A^(-144)
-        } else {  // counter - 36 blocks (256-bit borrow)
-            u64 b = CAP / 4;
-            for (int i = 0; i < 4; i++) {
-                const u64 o = base[i];
-                base[i] = o - b;
-                b = o < b ? 1 : 0;
-            }
-        }
-        u64 chk[32], w[CAP];
-        memcpy(chk, base, sizeof chk);
-        rs::engine_generate(e, chk, w, CAP);
-        if (memcmp(w, s->buf, sizeof w) != 0) return RS_ERR_UNSUPPORTED;  // not a refill of this engine
-        skip = (u64)s->cursor;
-    }
-    if (!rsk::tile_kernels(e, fam, 0).count) return RS_ERR_UNSUPPORTED;
-    const double ww = (double)n * r.words_per_sample;
-    const u64 words = skip + (u64)(ww * 1.01 + 16.0 * std::sqrt(ww) + 4096.0);
-    const u64 nwt = (words + WT_WORDS - 1) / WT_WORDS;
-    const u64 nblk = (nwt + WT_BLK - 1) / WT_BLK;
-    if (nblk > 0xFFFFFFFFULL) return RS_ERR_UNSUPPORTED;
-    int fold = 0;
-    if (e == RS_ENG_PHILOX) {
-        const u64 blocks = nwt * (WT_WORDS / 4);
-        fold = base[0] + blocks >= base[0] ? 1 : 0;  // counter word 0 never carries in the fill
-    }
-    const rsk::TileLaunch tl = rsk::tile_kernels(e, fam, fold);
-    // scratch: tables [nwt] 32 B, prefixes [nwt] 48 B, block tables / entries, ctl, pcg64 states
-    const size_t o_pre = nwt * sizeof(WTTab), o_blk = o_pre + nwt * sizeof(WTTab32);
-    const size_t o_in = o_blk + nblk * sizeof(WTTab32), o_ctl = o_in + nblk * 16, o_pcg = o_ctl + 64;
-    const size_t need = o_pcg + (e == RS_ENG_PCG64 ? nwt * 16 : 0);
-    if (need > c.tile_bytes) {
-        cudaFree(c.tile_buf);
-        c.tile_buf = nullptr;
-        c.tile_bytes = 0;
-        CK(cudaMalloc(&c.tile_buf, need));
-        c.tile_bytes = need;
-    }
-    char *tb = (char *)c.tile_buf;
-    WTPlan p;
-    memset(&p, 0, sizeof p);
-    p.engine = e;
-    p.kind = r.kind;
-    p.fm = s->full_mantissa;
-    p.n = n;
-    p.skip = skip;
-    p.nwt = nwt;
-    for (int i = 0; i < 6; i++) p.base[i] = base[i];
-    memcpy(p.fp, r.fp, sizeof p.fp);
-    memcpy(p.ip, r.ip, sizeof p.ip);
-    p.zslow = (r.table == 0 || r.table == 1) ? c.zslow[r.table] : nullptr;
-    p.zfast = (r.table == 0 || r.table == 1) ? c.zfast[r.table] : nullptr;
-    p.out = dout;
-    p.tab = (WTTab *)tb;
-    p.pre = (WTTab32 *)(tb + o_pre);
-    p.blk = (WTTab32 *)(tb + o_blk);
-    p.blk_in = (u64 *)(tb + o_in);
-    p.nblk = (u32)nblk;
-    p.ctl = (u32 *)(tb + o_ctl);
-    p.res = c.res;
-    CK(cudaMemsetAsync(p.ctl, 0, 64, st));
-    CK(cudaMemsetAsync(c.res, 0, offsetof(DevResult, serial_state), st));
-    rs_status rc;
-    if (e == RS_ENG_PHILOX) {
-        for (int i = 0; i < 10; i++) {  // round keys k + r W (counter.py:95-96)
-            p.rk0[i] = base[4] + (u64)i * 0x9E3779B97F4A7C15ULL;
-            p.rk1[i] = base[5] + (u64)i * 0xBB67AE8584CAA73BULL;
-        }
-    } else {
-        const u128 inc = ((u128)base[3] << 64) | base[2];
-        if (!c.have_lane || c.lane_inc[0] != base[2] || c.lane_inc[1] != base[3]) {
-            u64 lt[4 * 32];
-            for (int l = 0; l < 32; l++) {  // A^(WT_W l), pcg.py:41-55
-                u128 m, a;
-                rs::pcg_affine(inc, (u128)WT_W * l, m, a);
-                lt[4 * l] = (u64)m; lt[4 * l + 1] = (u64)(m >> 64);
-                lt[4 * l + 2] = (u64)a; lt[4 * l + 3] = (u64)(a >> 64);
-            }
-            if (!c.pcg_lane) CK(cudaMalloc(&c.pcg_lane, sizeof lt));
-            CK(cudaMemcpy(c.pcg_lane, lt, sizeof lt, cudaMemcpyHostToDevice));
-            c.lane_inc[0] = base[2];
-            c.lane_inc[1] = base[3];
-            c.have_lane = true;
-        }
-        // base state + A^(WT_WORDS 2^j), j < 40, for the warp-tile states
-        u64 *up = c.up_host;
-        for (int i = 0; i < 4; i++) up[i] = base[i];
-        for (int j = 0; j < 40; j++) {
-            u128 m, a;
-            rs::pcg_affine(inc, (u128)WT_WORDS << j, m, a);
-            up[4 + 4 * j] = (u64)m; up[5 + 4 * j] = (u64)(m >> 64);
-            up[6 + 4 * j] = (u64)a; up[7 + 4 * j] = (u64)(a >> 64);
-        }
-        CK(cudaMemcpyAsync(c.up_dev, up, (4 + 160) * 8, cudaMemcpyHostToDevice, st));
-        u64 *states = (u64 *)(tb + o_pcg);
-        const u64 *bp = c.up_dev, *pw = c.up_dev + 4;
-        u64 nn = nwt;
-        void *ka[] = {&bp, &pw, &states, &nn};
-        if ((rc = launch(rsk::pcg_wt_kernel(), dim3((unsigned)((nwt + 255) / 256)), dim3(256), ka, st))) return rc;
-        p.pcg_lane = c.pcg_lane;
-        p.pcg_wt = states;
-    }
-    void *args[] = {&p};
-    const u64 gc = (u64)c.sms * (u64)occupancy(tl.count);
-    if ((rc = launch(tl.count, dim3((unsigned)std::min<u64>(gc, (nwt + 7) / 8)), dim3(256), args, st))) return rc;
-    const size_t scan_smem = 2 * WT_BLK * 40;
-    CK(cudaFuncSetAttribute(rsk::wt_scan1_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem));
-    CK(cudaFuncSetAttribute(rsk::wt_scan2_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem));
-    if ((rc = launch(rsk::wt_scan1_kernel(), dim3((unsigned)nblk), dim3(WT_BLK), args, st, scan_smem))) return rc;
-    if ((rc = launch(rsk::wt_scan2_kernel(), dim3(1), dim3(WT_BLK), args, st, scan_smem))) return rc;
-    const u64 ge = (u64)c.sms * (u64)occupancy(tl.emit, tl.emit_smem);
-    if ((rc = launch(tl.emit, dim3((unsigned)std::min<u64>(ge, (nwt + 7) / 8)), dim3(256), args, st, tl.emit_smem)))
-        return rc;
-    CK(cudaMemcpyAsync(c.res_host, c.res, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
-    u32 *ctl_host = (u32 *)(c.up_host + 200);
-    CK(cudaMemcpyAsync(ctl_host, p.ctl, 16, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    const u64 total = ((u64)ctl_host[3] << 32) | ctl_host[2];
-    if (ctl_host[0] || ctl_host[1] || total < n) return RS_ERR_UNSUPPORTED;  // the two-pass path redoes it
-    E = c.res_host->end_pos - skip;
-    for (int i = 0; i < 6; i++) tal[i] = c.res_host->tally[i];
-    return RS_OK;
-}
-
 // The device part of one fill. On return (sync=true) `E` holds the stream units
 // consumed (64-bit words, or 32-bit halves incl. a used pending half when r.unit == 2)
 // and `tal` the tallies.
@@ -994,23 +801,12 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
         const void *fn = fixed_kernel(s->engine, r.fixed_mode);
         rc = plan_segments(c, p, p.weng ? p.weng : 1, 64, occupancy(fn, FX_SMEM), st, true, 144);
         if (rc) return rc;
-        // logical words whose output is complete (half modes: both halves; a trailing low
-        // half and the pending half stay on the element-store path)
-        const u64 wfull = u == 2 ? (p.pending_used ? 0 : n / 2) : n;
-        if ((rc = launch_fixed(c, p, fn, wfull, st))) return rc;
+        if ((rc = launch_fixed(c, p, fn, st))) return rc;
         E = n;
         chunks = 1;
         return RS_OK;
     }
 
-    if (sync) {  // the single-pass tile parse where it applies (counter / affine engines)
-        rc = run_tile(c, s, r, n, dout, st, E, tal);
-        if (rc != RS_ERR_UNSUPPORTED) {
-            chunks = 1;
-            return rc;
-        }
-        rs::clear_error();
-    }
     // variable consumption: chunks of provisioned words until n samples exist.
     // Chunk coordinates: chunk-local position lp in units; chunk 1 starts with the
     // pending half (u = 2) and the P buffered words, then the engine; a later chunk
@@ -1342,14 +1138,7 @@ rs_status rs_fill_streams(int32_t engine, const uint64_t *seed, int32_t n_seed, 
     // smaller tile keeps 2^16 streams in one wave
     if (d == FAM_LEMIRE && a.ip[1] > (1ULL << 60)) d = FAM_LEMIRE_RING;
     const void *fn = rsk::streams_kernel(engine, d);
-    // 8-byte rows as a 2-D tensor (row = stream) for the TMA store path
-    CUtensorMap tm;
-    memset(&tm, 0, sizeof tm);
-    a.tma = 0;
-    if (getenv("RS_TMA") && elem_size(dist) == 8 && n_per_stream % 2 == 0 && d != FAM_LEMIRE_RING &&
-        !(d == FAM_FIXED && (r.fixed_mode == FX_U01F || r.fixed_mode == FX_HMAP)))
-        a.tma = make_row_tmap(&tm, sg.dptr, n_per_stream, n_streams) ? 1 : 0;
-    void *args[] = {&a, &tm};
+    void *args[] = {&a};
     unsigned g2 = (unsigned)((n_streams + STR_BLOCK - 1) / STR_BLOCK);
     if ((rc = launch(fn, dim3(g2), dim3(STR_BLOCK), args, st, d == FAM_LEMIRE_RING ? ST_SMEM_RING : ST_SMEM)))
         return rc;

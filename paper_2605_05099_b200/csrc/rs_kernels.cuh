@@ -4,7 +4,6 @@
 // below, and by the host translation unit rs_fill.cu (types only). Split so the
 // ~240 kernels compile in parallel.
 #pragma once
-#include <cuda.h>  // CUtensorMap (TMA tensor stores)
 #include <cuda_runtime.h>
 
 #include <type_traits>
@@ -52,8 +51,6 @@ struct FillPlan {
     u64 lanes[32];                // interleaved engines: the 8 lane states (lane-major)
     u64 G, Gpad;                  // interleaved fixed fills: step groups (real / padded)
     int vec_ok;                   // counter-based fill: outputs 32-byte aligned per block
-    int tma;                      // k_fixed: warps whose 32 segments are full rows store through TMA
-    u64 tma_rows;                 // full segments (rows of the tensor map)
     double fp[4];
     u64 ip[4];
     GammaPrm ga, gb;
@@ -92,50 +89,6 @@ struct FillPlan {
     u32 *c1own;                   // phase-1 samples before the merge (all of them if none)
     u32 *mrank0;                  // phase-0 sample index at the merge point
 };
-// ----------------------------------------------------------------------------- warp-tile parse
-// (k_tile.cu) Counter / affine engines (Philox, PCG64) reach any word directly, so the
-// stream is cut into warp-tiles of 512 consecutive words (32 lanes x 16), each parsed by
-// one warp with no dependence on any other: a count pass tabulates each warp-tile's
-// (exit, count) for entries 0..7, two small scans compose the tables, and the emit pass
-// parses each warp-tile from its exact entry and writes its samples with a bulk copy.
-struct DevResult;
-constexpr int WT_W = 16;                       // words per lane window
-constexpr u64 WT_WORDS = 32 * WT_W;            // words per warp-tile
-constexpr int WT_D = 8;                        // tabulated entries 0..WT_D-1
-constexpr int WT_BLK = 1024;                   // warp-tiles per scan block
-struct WTTab {                                 // a warp-tile's table (K1), 32 B
-    u32 x[2];                                  // exits (bytes) for entries 0..7; 0xFF: undefined
-    u32 c[4];                                  // counts (u16 pairs)
-    u32 pad[2];
-};
-struct WTTab32 {                               // composed tables (scans), 48 B
-    u32 x[2];
-    u32 c[WT_D];
-    u32 pad[2];
-};
-struct WTPlan {
-    int engine, kind, fm, pad;
-    u64 n;                                     // samples
-    u64 skip;                                  // raw word where the logical stream (sample 0) starts
-    u64 nwt;                                   // warp-tiles
-    u64 base[6];                               // rewound engine: pcg64 slo, shi, ilo, ihi; philox c0-c3, k0, k1
-    u64 rk0[10], rk1[10];                      // philox round keys
-    const u64 *pcg_lane;                       // [32][4]: A^(WT_W l) as (mul lo, hi, add lo, hi)
-    const u64 *pcg_wt;                         // [nwt][2]: the state at raw word WT_WORDS w
-    double fp[4];
-    u64 ip[4];
-    const RsZigSlow *zslow;
-    const ZigFast *zfast;
-    void *out;
-    WTTab *tab;                                // [nwt]
-    WTTab32 *pre;                              // [nwt] exclusive in-block prefix tables
-    WTTab32 *blk;                              // [nblk] block tables
-    u64 *blk_in;                               // [nblk][2] exact (entry, offset) entering each block
-    u32 nblk;
-    u32 *ctl;                                  // [0] undefined entry, [1] parse mismatch; [2..3] total (u64)
-    DevResult *res;
-};
-
 // per-sample tally word of the gamma attempt machine: gamma attempts (8 bits), normal
 // attempts (12), normal pdf evaluations (12); 0xFFFFFFFF never occurs (flagged instead)
 __device__ __forceinline__ bool pack_tally(u32 ga, u32 na, u32 np, u32 &w) {
@@ -1188,8 +1141,7 @@ constexpr int LR_ROW = 65;  // per-stream Lemire rows: a 64-sample ring per lane
 // LDS.128) measured slower -- 1.80 vs 1.51 ms for x256** 2^30 -- because its per-word
 // address arithmetic lands on the ALU pipe, which the xoshiro step already fills (74 %).
 constexpr int FX_ROW = FX_CH + 1;
-constexpr size_t FX_SMEM = (size_t)(BLOCK / 32) * 8704;  // dynamic shared memory of k_fixed (>= the tile,
-                                                           // 8 KB TMA boxes and 34-word bulk rows per warp)
+constexpr size_t FX_SMEM = (size_t)(BLOCK / 32) * 32 * FX_ROW * 8;  // dynamic shared memory of k_fixed
 __device__ __forceinline__ u32 fx_at(u32 l, u32 j) { return l * FX_ROW + j; }
 template <int E, int MODE>
 __device__ __forceinline__ void write_run(const FillPlan &p, Src<E> &s, u64 *out, u64 first, u64 last,
@@ -1234,98 +1186,9 @@ __device__ __forceinline__ void write_run(const FillPlan &p, Src<E> &s, u64 *out
         for (; i < last; i++) out[i] = fx_map<MODE>(p, s.e.next());
 }
 
-// ---- TMA tensor stores (Blackwell store path). The output is viewed as a 2-D tensor whose
-// rows are the threads' segments (row t = the L words of segment t, row stride L words), so
-// a warp's next 32 words per lane form a 32-row x 32-column box. Lanes write their words
-// into two 32 x 16-word boxes in shared memory in the TMA 128-byte swizzle (16-byte chunk c
-// of row r at c ^ (r & 7): each quarter-warp's STS.128 hits 8 distinct bank groups), and
-// lane 0 stores both with cp.async.bulk.tensor (SASS UTMASTG): one instruction per 8 KB
-// instead of the tile read-back (LDS + STG.128 by every lane, 2-way bank-conflicted).
-__device__ __forceinline__ u32 sw128(u32 row, u32 col) {  // byte offset of word `col` (< 16) in a box row
-    return row * 128 + ((((col >> 1) ^ (row & 7)) << 4) | ((col & 1) << 3));
-}
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap *tm, const void *smem, int c0, int c1) {
-    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tm),
-                 "r"((unsigned)__cvta_generic_to_shared(smem)), "r"(c0), "r"(c1) : "memory");
-}
-// One 32-row x 16-word box: lanes write their 16 words (8 STS.128 pairs, 128-byte swizzle),
-// then lane 0 issues the tensor store as its own bulk group. Box h (0/1) of a warp is
-// rewritten only after its previous store has been read (wait_group.read 1: the other box
-// may still be in flight), so generation of one box overlaps the store of the other.
-// STATIC: the word source has no divergent loop (fixed maps): a fully unrolled pair loop
-template <bool STATIC, class F>
-__device__ __forceinline__ void tma_box(const CUtensorMap *tm, unsigned char *boxh, int col, int row0, bool wait,
-                                        F word) {
-    const u32 lane = threadIdx.x & 31;
-    if (wait) {
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        __syncwarp();
-    }
-    const unsigned rb = (unsigned)__cvta_generic_to_shared(boxh) + lane * 128, x7 = (lane & 7) << 4;
-    if constexpr (STATIC) {
-#pragma unroll
-        for (u32 pr = 0; pr < 8; pr++) {
-            const u64 a = word(), b = word();
-            asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(rb + ((pr << 4) ^ x7)), "l"(a), "l"(b) : "memory");
-        }
-    } else {  // pairs 0..7 of the row, a per-lane bound (see stream_rows8_tma)
-        for (u32 q = lane; q < lane + 8; q++) {
-            const u32 pr = q - lane;
-            const u64 a = word(), b = word();
-            asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(rb + ((pr << 4) ^ x7)), "l"(a), "l"(b) : "memory");
-        }
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
-    if (lane == 0) {
-        tma_store_2d(tm, boxh, col, row0);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    }
-}
-__device__ __forceinline__ void tma_drain() {
-    if ((threadIdx.x & 31) == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    __syncwarp();
-}
-// Per-lane 1-D bulk copies instead (RS_TMA=2): lane l owns a 16-byte-aligned 272-byte row
-// (34-word stride: its STS.128 pairs hit 8 distinct bank groups per quarter-warp), fences its
-// own writes and copies its 256 bytes with cp.async.bulk (UBLKCP); no warp synchronisation.
-template <int E, int MODE, class PL, class SRC>
-__device__ __forceinline__ void write_run_bulk(const PL &p, SRC &s, u64 *gout, u64 nchunk, u64 L,
-                                               unsigned char *tile) {
-    const u32 lane = threadIdx.x & 31;
-    const unsigned rb = (unsigned)__cvta_generic_to_shared(tile) + lane * 272;
-    for (u64 k = 0; k < nchunk; k++) {
-        if (k > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-#pragma unroll
-        for (u32 pr = 0; pr < 16; pr++) {
-            const u64 a = fx_map<MODE>(p, s.next()), b = fx_map<MODE>(p, s.next());
-            asm volatile("st.shared.v2.b64 [%0], {%1, %2};" ::"r"(rb + 16 * pr), "l"(a), "l"(b) : "memory");
-        }
-        const u64 c0 = 32 * k, nw = L - c0 < 32 ? L - c0 : 32;  // the row's last chunk may be 16 words
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gout + c0), "r"(rb),
-                     "r"((unsigned)(nw * 8)) : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    }
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-
-// nchunk chunks of 32 words per lane; the warp's rows are row0 .. row0 + 31 (all full)
-template <int E, int MODE, class PL, class SRC>
-__device__ __forceinline__ void write_run_tma(const PL &p, SRC &s, const CUtensorMap *tm, u64 row0, u64 nchunk,
-                                              unsigned char *box) {
-    auto word = [&]() { return fx_map<MODE>(p, s.next()); };
-    for (u64 k = 0; k < nchunk; k++) {
-        tma_box<E != RS_ENG_RANLUX>(tm, box, (int)(32 * k), (int)row0, k > 0, word);
-        tma_box<E != RS_ENG_RANLUX>(tm, box + 4096, (int)(32 * k + 16), (int)row0, true, word);
-    }
-    tma_drain();
-}
-
 template <int E, int MODE>
-__global__ void __launch_bounds__(BLOCK) k_fixed(const __grid_constant__ FillPlan p,
-                                                 const __grid_constant__ CUtensorMap tm) {
-    extern __shared__ __align__(1024) u64 fx_dyn[];  // FX_SMEM
+__global__ void __launch_bounds__(BLOCK) k_fixed(const __grid_constant__ FillPlan p) {
+    extern __shared__ __align__(16) u64 fx_dyn[];  // FX_SMEM
     u64 *tile = fx_dyn + (threadIdx.x >> 5) * 32 * FX_ROW;
     u32 t = blockIdx.x * BLOCK + threadIdx.x;
     // every lane of a warp takes part in the tile stores; idle lanes just contribute nothing
@@ -1339,22 +1202,6 @@ __global__ void __launch_bounds__(BLOCK) k_fixed(const __grid_constant__ FillPla
     if (t < p.T) make_engine<E>(p, t, s.e);
     s.pre = p.prefix;
     s.npre = t == 0 ? p.P : 0;
-    // warps whose 32 segments are all full rows of the tensor map store through TMA
-    const u64 row0 = (u64)(t & ~31u);
-    if (p.tma && row0 + 32 <= p.tma_rows) {
-        if (t == 0) {  // the buffered prefix precedes row 0 (the tensor starts at the engine words)
-            u64 *out = (u64 *)p.out;
-            for (int i = 0; i < p.P; i++) out[i] = fx_map<MODE>(p, p.prefix[i]);
-            s.npre = 0;
-        }
-        // tensor boxes need 1024-byte alignment (128-byte swizzle atoms); bulk rows 16 bytes
-        unsigned char *box = (unsigned char *)fx_dyn + (size_t)(threadIdx.x >> 5) * (p.tma == 2 ? 8704 : 8192);
-        if (p.tma == 2)
-            write_run_bulk<E, MODE>(p, s, (u64 *)p.out + p.P + (u64)t * p.L, (p.L + 31) / 32, p.L, box);
-        else
-            write_run_tma<E, MODE>(p, s, &tm, row0, (p.L + 31) / 32, box);
-        return;
-    }
     if constexpr (!is_half(MODE)) {
         u64 *out = (u64 *)p.out;
         if (t == 0 && last > p.n) last = p.n;  // n < P: prefix only
@@ -1653,7 +1500,6 @@ struct StreamArgs {
     const ZigFastF *zfastf;
     const u64 *rlx_A;
     void *out;
-    int tma;  // rows are a 2-D tensor map (k_streams' second parameter)
 };
 
 template <class EN>
@@ -1708,23 +1554,6 @@ __device__ void seed_fe128(const StreamArgs &a, u64 j, u64 *out, int nout) {
 // same length): each lane fills 32 outputs of its row into its row of the warp tile,
 // then the warp stores two lanes' 256-byte chunks per STG.128 instruction (the fixed
 // fills' pattern, write_run). produce() returns the lane's next output as bits.
-// The same rows through TMA: the output is a 2-D tensor (row = stream, nper words), each
-// 32-sample chunk of the warp's 32 streams two 32 x 16 boxes (write_run_tma's layout).
-// tma_box's pair loop runs from `lane` to lane + 8 (the same 8 steps everywhere, but a
-// per-lane bound: the sampler's rejection loop inside produce() must not share a uniform
-// counter with it).
-template <class F>
-__device__ __forceinline__ void stream_rows8_tma(u64 *out, u64 j, u64 nper, const CUtensorMap *tm, u64 row0,
-                                                 unsigned char *box, F produce) {
-    const u64 nch = nper / FX_CH;
-    for (u64 k = 0; k < nch; k++) {
-        tma_box<false>(tm, box, (int)(32 * k), (int)row0, k > 0, produce);
-        tma_box<false>(tm, box + 4096, (int)(32 * k + 16), (int)row0, true, produce);
-    }
-    tma_drain();
-    for (u64 i = nch * FX_CH; i < nper; i++) out[j * nper + i] = produce();
-}
-
 template <class F>
 __device__ __forceinline__ void stream_rows8(u64 *out, u64 j, u64 nper, bool valid, u64 *tile, F produce) {
     const u32 lane = threadIdx.x & 31;
@@ -1820,12 +1649,10 @@ __device__ __forceinline__ void stream_rows_lemire(u64 *out, u64 j, u64 nper, bo
 // 64-thread blocks: one thread per stream cannot be split (sfc64 has no skip-ahead), so
 // small blocks spread the few warps evenly over the SMs (2^16 streams: 13.8 warps/SM)
 constexpr int STR_BLOCK = 64;
-constexpr size_t ST_SMEM = (size_t)(STR_BLOCK / 32) * 32 * FX_ROW * 8 + 1024;  // dynamic shared memory of k_streams
-                                                                              // (>= 8 KB TMA boxes per warp)
+constexpr size_t ST_SMEM = (size_t)(STR_BLOCK / 32) * 32 * FX_ROW * 8;   // dynamic shared memory of k_streams
 constexpr size_t ST_SMEM_RING = (size_t)(STR_BLOCK / 32) * 32 * LR_ROW * 8;  // ... with a.ring
 template <int E, int D>
-__global__ void __launch_bounds__(STR_BLOCK) k_streams(const __grid_constant__ StreamArgs a,
-                                                       const __grid_constant__ CUtensorMap tm) {
+__global__ void __launch_bounds__(STR_BLOCK) k_streams(const __grid_constant__ StreamArgs a) {
     __shared__ ZigFast sm[256];
     if (a.zfast) {
         for (int i = threadIdx.x; i < 256; i += blockDim.x) sm[i] = a.zfast[i];
@@ -1836,7 +1663,7 @@ __global__ void __launch_bounds__(STR_BLOCK) k_streams(const __grid_constant__ S
     u64 j = (u64)blockIdx.x * STR_BLOCK + threadIdx.x;
     // 8-byte rows through the warp tile (whole warps: no early exit) when every row
     // start is 16-byte aligned; otherwise the per-thread writers below
-    extern __shared__ __align__(1024) u64 st_dyn[];  // ST_SMEM
+    extern __shared__ __align__(16) u64 st_dyn[];  // ST_SMEM
     constexpr bool W8 = sizeof(typename DistOf<(D == FAM_FIXED || D == FAM_LEMIRE_RING) ? FAM_LEMIRE : D>::type::out_t) == 8;
     const bool tiled = W8 && !(D == FAM_FIXED && is_half(a.fmode)) && a.nper % 2 == 0 &&
                        (((uintptr_t)a.out) & 15) == 0;
@@ -1887,15 +1714,7 @@ __global__ void __launch_bounds__(STR_BLOCK) k_streams(const __grid_constant__ S
     // STG.256 per 32-byte group). Its round-1 fault here was a uniform-register hazard in
     // the writer's address arithmetic under divergence, not the ring (rs_device.cuh run
     // writers, DESIGN 7); the writers now carry per-thread group pointers.
-    // a warp whose 32 streams are all rows of the tensor map stores through TMA
-    const u64 row0 = j & ~31ULL;
-    const bool tma = tiled && a.tma && row0 + 32 <= a.nstreams;
-    unsigned char *box = (unsigned char *)st_dyn + (size_t)(threadIdx.x >> 5) * 8192;
     if constexpr (D == FAM_FIXED) {  // raw / uniform / masked laws: a fresh stream, no pending half
-        if (tma) {
-            stream_rows8_tma((u64 *)a.out, j, a.nper, &tm, row0, box, [&]() { return fx_map_rt(a, e.next()); });
-            return;
-        }
         if (tiled) {
             stream_rows8((u64 *)a.out, j, a.nper, valid, tile, [&]() { return fx_map_rt(a, e.next()); });
             return;
@@ -1933,15 +1752,13 @@ __global__ void __launch_bounds__(STR_BLOCK) k_streams(const __grid_constant__ S
                     while (!d.accept(e.next(), o)) {}
                     return o;
                 };
-                if (tma) stream_rows8_tma((u64 *)a.out, j, a.nper, &tm, row0, box, prod);
-                else stream_rows8((u64 *)a.out, j, a.nper, valid, tile, prod);
+                stream_rows8((u64 *)a.out, j, a.nper, valid, tile, prod);
             } else {  // 8-byte samplers are word-fed
                 auto prod = [&]() {
                     T v = d.sample(e, tl);
                     return *(u64 *)&v;
                 };
-                if (tma) stream_rows8_tma((u64 *)a.out, j, a.nper, &tm, row0, box, prod);
-                else stream_rows8((u64 *)a.out, j, a.nper, valid, tile, prod);
+                stream_rows8((u64 *)a.out, j, a.nper, valid, tile, prod);
             }
             return;
         }
@@ -1995,14 +1812,6 @@ const void *streams_kernel(int engine, int fam); // k_streams_a.cu (dispatch), k
 const void *streams_kernel_b(int engine, int fam);
 const void *serial_kernel(int engine, int fam, int fixed_mode);  // k_misc.cu
 const void *setup_kernel();     // k_misc.cu: k_x256_setup
-struct TileLaunch {  // k_tile.cu: warp-tile parse for philox / pcg64 (norm, exp, Lemire)
-    const void *count, *emit;
-    size_t emit_smem;
-};
-TileLaunch tile_kernels(int engine, int fam, int fold);  // count == nullptr: not covered
-const void *pcg_wt_kernel();   // per-warp-tile pcg64 states
-const void *wt_scan1_kernel(); // in-block scans of the tables
-const void *wt_scan2_kernel(); // block chain
 struct MvnLaunch {  // k_mvn.cu: the FP64 tensor-core contraction X = mean + z L^T
     const void *fn;
     size_t smem;
