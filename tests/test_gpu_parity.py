@@ -746,3 +746,28 @@ def test_mvn_indefinite_covariance_consumes_nothing():
     ref = o.fill("norm", {}, 5000)
     got = r.fill("norm", {}, 5000).cpu().numpy()
     assert np.array_equal(_bits(got), _bits(ref))
+
+
+@pytest.mark.parametrize("engine,dist,params", [("x256**", "norm", {}), ("pcg64", "gamma", {"alpha": 2.5}),
+                                                ("philox", "u01f", {}), ("sfc64", "uint64", {"b": 1000003})])
+def test_integration_device_fill(engine, dist, params):
+    """integration.device_fill / device_mvn on a generator with the reference's structure
+    (engine.get_state/set_state, buffer.capture/restore, flags, counters): the same values
+    as the oracle and the same post-fill position written back."""
+    from paper_2605_05099_b200 import integration
+    ref_like = state_io.create(engine, seed=[77])
+    o = O.OracleRng(engine, seed=[77])
+    for _ in range(3):  # mid-buffer, with a pending half
+        assert ref_like.next_u32() == o.next_u32()
+    vals = integration.device_fill(ref_like, dist, params, 5000)
+    assert isinstance(vals, list) and len(vals) == 5000
+    ref = o.fill(dist, params, 5000)
+    assert np.array_equal(_bits(np.asarray(vals, dtype=ref.dtype)), _bits(ref))
+    _assert_same_position(ref_like, o)
+    d = 8
+    S = np.eye(d) + 0.1
+    X = integration.device_mvn(ref_like, np.zeros(d), S, n=256)
+    z = o.fill("stdnorm", {}, 256 * d).reshape(256, d)
+    Lf = np.linalg.cholesky(S)
+    assert np.max(np.abs(X - z @ Lf.T) / (np.abs(z) @ np.abs(Lf).T)) <= 1e-12
+    _assert_same_position(ref_like, o)
