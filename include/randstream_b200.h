@@ -194,7 +194,7 @@ typedef struct rs_range_info {
     uint64_t count;            /* samples starting in [entry, units(slice)) */
     uint64_t exit;             /* first sample boundary at or past the slice end, in units past it */
     uint64_t end_pos;          /* after rs_range_emit(keep > 0): unit position (from the slice start)
-                                  right after sample keep-1; else entry */
+                                  right after sample keep-1; else the slice's entry */
     uint64_t tally[6];         /* emitted samples' tallies (rs_fill_result layout) */
     int32_t unit;
     int32_t resync_rounds;
@@ -209,6 +209,14 @@ rs_status rs_range_geometry(int32_t engine, int32_t dist, const double *fparams,
 rs_status rs_range_count(const rs_stream *stream, int32_t dist, const double *fparams,
                          const uint64_t *iparams, uint64_t entry, uint64_t seg_len, uint32_t n_seg,
                          rs_range_info *info, void *cuda_stream);
+/* rs_range_count with the entry guess folded in: `window_start` is positioned n_warm segments
+ * (n_warm a multiple of 256) before the slice; the plan parses window + slice in the same
+ * launches, assuming a sample starts at the window start, and the slice enters at the
+ * window's exit (returned in info->end_pos). Saves the separate warm-up count's launches and
+ * host round trip. The emitted samples and positions are those of rs_range_count(entry). */
+rs_status rs_range_count_warm(const rs_stream *window_start, int32_t dist, const double *fparams,
+                              const uint64_t *iparams, uint32_t n_warm, uint64_t seg_len, uint32_t n_seg,
+                              rs_range_info *info, void *cuda_stream);
 /* write the first `keep` samples of the counted slice into device memory (synchronous).
  * Any other fill on the device between count and emit invalidates the slice (RS_ERR_VALUE). */
 rs_status rs_range_emit(uint64_t keep, void *out_device, rs_range_info *info, void *cuda_stream);

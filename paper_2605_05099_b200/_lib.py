@@ -116,8 +116,10 @@ def _load():
                                     ctypes.POINTER(ctypes.c_uint32)]
     L.rs_range_count.argtypes = [ctypes.POINTER(RsStream), ctypes.c_int32, DBLP, U64P, ctypes.c_uint64,
                                  ctypes.c_uint64, ctypes.c_uint32, ctypes.POINTER(RsRangeInfo), ctypes.c_void_p]
+    L.rs_range_count_warm.argtypes = [ctypes.POINTER(RsStream), ctypes.c_int32, DBLP, U64P, ctypes.c_uint32,
+                                      ctypes.c_uint64, ctypes.c_uint32, ctypes.POINTER(RsRangeInfo), ctypes.c_void_p]
     L.rs_range_emit.argtypes = [ctypes.c_uint64, ctypes.c_void_p, ctypes.POINTER(RsRangeInfo), ctypes.c_void_p]
-    for name in ("rs_dist_info", "rs_range_geometry", "rs_range_count", "rs_range_emit"):
+    for name in ("rs_dist_info", "rs_range_geometry", "rs_range_count", "rs_range_count_warm", "rs_range_emit"):
         getattr(L, name).restype = ctypes.c_int
     for name in ("rs_init_device", "rs_seed_words", "rs_engine_seed", "rs_engine_seed_from", "rs_engine_check_state",
                  "rs_engine_generate", "rs_engine_jump", "rs_engine_advance_words", "rs_pcg_advance", "rs_fill",
@@ -135,7 +137,7 @@ EXPORTED = (
     "rs_engine_seed_words", "rs_engine_chunk", "rs_seed_words", "rs_engine_seed", "rs_engine_seed_from",
     "rs_engine_check_state", "rs_engine_generate", "rs_engine_jump", "rs_engine_advance_words", "rs_pcg_advance",
     "rs_fill", "rs_fill_async", "rs_fill_streams", "rs_mvn", "rs_mvn_apply",
-    "rs_dist_info", "rs_range_geometry", "rs_range_count", "rs_range_emit",
+    "rs_dist_info", "rs_range_geometry", "rs_range_count", "rs_range_count_warm", "rs_range_emit",
 )
 
 

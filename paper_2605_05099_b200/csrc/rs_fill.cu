@@ -78,6 +78,8 @@ struct DevCtx {
         u64 count = 0;
         int unit = 1;
         bool mem = false;
+        u64 origin = 0;  // units from the plan start to the slice start (warm-up segments)
+        u64 entry = 0;   // the slice's entry (units from the slice start)
     } range;
 };
 
@@ -1312,9 +1314,13 @@ rs_status rs_range_geometry(int32_t engine, int32_t dist, const double *fparams,
     return RS_OK;
 }
 
-rs_status rs_range_count(const rs_stream *s, int32_t dist, const double *fparams, const uint64_t *iparams,
-                         uint64_t entry, uint64_t seg_len, uint32_t n_seg, rs_range_info *info, void *cuda_stream) {
-    std::lock_guard<std::mutex> g(g_mu);
+// count + exit of a slice of n_seg segments that follows n_warm warm-up segments (n_warm = 0:
+// the slice alone, entering at `entry`; n_warm > 0: the plan starts at the warm-up window,
+// whose first segment is assumed to start a sample, and the count / fixup passes resolve
+// the slice's entry from the window's exit in the same launches)
+static rs_status range_count_core(const rs_stream *s, int32_t dist, const double *fparams, const uint64_t *iparams,
+                                  uint64_t entry, uint32_t n_warm, uint64_t seg_len, uint32_t n_seg, rs_range_info *info,
+                                  void *cuda_stream) {
     rs_status rc = check_stream(s);
     if (rc) return rc;
     double fz[4] = {0, 0, 0, 0};
@@ -1329,8 +1335,9 @@ rs_status rs_range_count(const rs_stream *s, int32_t dist, const double *fparams
         rs::set_error("a range fill starts at a fresh stream position (no buffered words)");
         return RS_ERR_VALUE;
     }
-    if (seg_len == 0 || seg_len % RS_RANGE_ALIGN || n_seg == 0 || n_seg % BLOCK) {
-        rs::set_error("range geometry: seg_len must be a multiple of 72 and n_seg of 256");
+    if (seg_len == 0 || seg_len % RS_RANGE_ALIGN || n_seg == 0 || n_seg % BLOCK || n_warm % BLOCK ||
+        (u64)n_warm + n_seg > 0xFFFFFFFFULL) {
+        rs::set_error("range geometry: seg_len must be a multiple of 72 and n_seg, n_warm of 256");
         return RS_ERR_VALUE;
     }
     const u64 u = (u64)r.unit;
@@ -1346,11 +1353,12 @@ rs_status rs_range_count(const rs_stream *s, int32_t dist, const double *fparams
     fill_plan_common(p, *c, r, s->engine, s->full_mantissa);
     memcpy(p.base, s->state, sizeof p.base);
     memcpy(p.lanes, s->state, sizeof p.lanes);
-    p.lp0 = entry;
+    p.lp0 = n_warm ? 0 : entry;
     p.n = 0;
+    const u32 Tall = n_warm + n_seg;
     VarKernels K = var_kernels(s->engine, r.family);
     const bool mem = parse_from_memory(s->engine);
-    if ((rc = plan_segments(*c, p, seg_len * n_seg, 0, 0, st, !mem, RS_RANGE_ALIGN, seg_len, n_seg))) return rc;
+    if ((rc = plan_segments(*c, p, seg_len * Tall, 0, 0, st, !mem, RS_RANGE_ALIGN, seg_len, Tall))) return rc;
     if ((rc = prep_chunk(*c, p, r, mem, st))) return rc;
     CK(cudaMemsetAsync(c->res, 0, offsetof(DevResult, serial_state), st));
     unsigned gdim = p.T / BLOCK;
@@ -1375,6 +1383,14 @@ rs_status rs_range_count(const rs_stream *s, int32_t dist, const double *fparams
         if ((rc = launch(K.fixup, dim3(gdim), dim3(BLOCK), a3, st))) return rc;
         u32 *tmp = ex_cur; ex_cur = ex_other; ex_other = tmp;
     }
+    u64 wentry = entry;
+    if (n_warm) {  // the warm-up segments emit nothing; the slice enters at the window's exit
+        CK(cudaMemsetAsync(c->cnt, 0, (size_t)n_warm * 8, st));
+        u32 e32 = 0;
+        CK(cudaMemcpyAsync(&e32, ex_cur + (n_warm - 1), 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        wentry = e32;
+    }
     size_t bytes = c->cub_bytes;
     CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->cnt, c->off, (int)p.T, st));
     u64 last_off = 0, last_cnt = 0;
@@ -1398,17 +1414,33 @@ rs_status rs_range_count(const rs_stream *s, int32_t dist, const double *fparams
     c->range.count = last_off + last_cnt;
     c->range.unit = r.unit;
     c->range.mem = mem;
+    c->range.origin = u * seg_len * (u64)n_warm;
+    c->range.entry = wentry;
     c->range.valid = true;
     if (info) {
         memset(info, 0, sizeof *info);
         info->count = last_off + last_cnt;
         info->exit = last_ex;  // seg_end(T-1) == units(slice): the exit is past the slice end
-        info->end_pos = entry;
+        info->end_pos = wentry;
         info->unit = r.unit;
         info->resync_rounds = rounds;
     }
     rs::clear_error();
     return RS_OK;
+}
+
+rs_status rs_range_count(const rs_stream *s, int32_t dist, const double *fparams, const uint64_t *iparams,
+                         uint64_t entry, uint64_t seg_len, uint32_t n_seg, rs_range_info *info, void *cuda_stream) {
+    std::lock_guard<std::mutex> g(g_mu);
+    return range_count_core(s, dist, fparams, iparams, entry, 0, seg_len, n_seg, info, cuda_stream);
+}
+
+rs_status rs_range_count_warm(const rs_stream *window_start, int32_t dist, const double *fparams,
+                              const uint64_t *iparams, uint32_t n_warm, uint64_t seg_len, uint32_t n_seg,
+                              rs_range_info *info, void *cuda_stream) {
+    std::lock_guard<std::mutex> g(g_mu);
+    if (n_warm == 0) { rs::set_error("rs_range_count_warm needs n_warm > 0 (else rs_range_count)"); return RS_ERR_VALUE; }
+    return range_count_core(window_start, dist, fparams, iparams, 0, n_warm, seg_len, n_seg, info, cuda_stream);
 }
 
 rs_status rs_range_emit(uint64_t keep, void *out_device, rs_range_info *info, void *cuda_stream) {
@@ -1423,7 +1455,7 @@ rs_status rs_range_emit(uint64_t keep, void *out_device, rs_range_info *info, vo
     if (keep > R.count) { rs::set_error("keep exceeds the range's sample count"); return RS_ERR_VALUE; }
     if (info) {
         info->count = R.count;
-        info->end_pos = R.p.lp0;
+        info->end_pos = R.entry;
         for (int i = 0; i < 6; i++) info->tally[i] = 0;
     }
     if (keep == 0) { rs::clear_error(); return RS_OK; }
@@ -1441,7 +1473,7 @@ rs_status rs_range_emit(uint64_t keep, void *out_device, rs_range_info *info, vo
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
     if (info) {
-        info->end_pos = c->res_host->end_pos;
+        info->end_pos = c->res_host->end_pos - R.origin;  // from the slice start
         for (int i = 0; i < 6; i++) info->tally[i] = c->res_host->tally[i];
     }
     rs::clear_error();

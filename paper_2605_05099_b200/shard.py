@@ -124,6 +124,19 @@ class DeviceRanges:
         DeviceRanges._slot[self.device.index] = self._token
         return int(res.count), int(res.exit), int(res.resync_rounds)
 
+    def count_warm(self, wrng, dist_id, fp, ip, n_warm, seg_len, n_seg):
+        """rs_range_count_warm: the slice counted behind n_warm warm-up segments in the same
+        launches (the entry guess without a separate warm-up count). -> (count, exit, entry, rounds)"""
+        res = _lib.RsRangeInfo()
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib.rs_range_count_warm(_byref(wrng.to_stream()), dist_id, _fp(fp), _ip(ip), int(n_warm),
+                                                    int(seg_len), int(n_seg), _byref(res), self._stream()))
+        # a re-count (emit after another slice ran on the device) goes through rs_range_count
+        self._args = (positioned(wrng, int(n_warm) * int(seg_len)), dist_id, fp, ip, int(res.end_pos), seg_len, n_seg)
+        self._token = object()
+        DeviceRanges._slot[self.device.index] = self._token
+        return int(res.count), int(res.exit), int(res.end_pos), int(res.resync_rounds)
+
     def emit(self, keep, out_dtype):
         if DeviceRanges._slot.get(self.device.index) is not self._token:
             self.count(*self._args)
@@ -227,6 +240,16 @@ class ShardedFill:
         """Steps 1-2: entry guess from the warm-up window, then count + exit of the slice."""
         g = self.rank
         self.slice_rng = positioned(self.rng, g * self.R)
+        if g > 0 and self.n and self.window[0] * self.window[1] and hasattr(self.ranges, "count_warm"):
+            # the warm-up window as leading segments of the slice's own plan (one count)
+            nw = -(-self.window[0] * self.window[1] // self.L)
+            nw = (nw + 255) // 256 * 256
+            if nw * self.L <= g * self.R:
+                wr = positioned(self.rng, g * self.R - nw * self.L)
+                self.cnt, self.exit, self.entry, rr = self.ranges.count_warm(wr, self.dist_id, self.fp, self.ip, nw,
+                                                                             self.L, self.T)
+                self.rounds += rr
+                return
         if g == 0 or self.n == 0 or self.window[0] * self.window[1] == 0:  # (0, 0): no warm-up, guess 0
             self.entry = 0
         else:
