@@ -21,6 +21,8 @@ KEEP_PREFIX = (
     "smsp__thread_inst_executed_per_inst_executed.ratio", "smsp__warps_active.avg.per_cycle_active",
     "sm__warps_active.avg.pct_of_peak_sustained_active",
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "launch__occupancy_limit_registers",
+    "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
     "l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_st.sum",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "sm__cycles_elapsed.avg.per_second",
 )
@@ -33,9 +35,10 @@ def main():
     ap.add_argument("out")
     ap.add_argument("--capture", required=True)
     ap.add_argument("--algorithmic-bytes", type=float, default=None)
+    ap.add_argument("--row", type=int, default=0, help="which captured launch (0 = first)")
     a = ap.parse_args()
     rows = list(csv.reader(open(a.raw)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units, vals = rows[0], rows[1], rows[2 + a.row]
     metrics = {}
     kernel = None
     for k, u, v in zip(hdr, units, vals):

@@ -27,7 +27,7 @@ a = ap.parse_args()
 params = {}
 for kv in a.params:
     k, v = kv.split("=")
-    params[k] = int(v) if k == "b" else float(v)
+    params[k] = int(v) if (k == "b" and a.dist == "uint64") else float(v)
 n = 1 << a.log2n
 r = state_io.create(a.engine, seed=[a.seed])
 r.set_full_mantissa(a.fm)
