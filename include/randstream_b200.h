@@ -170,6 +170,17 @@ rs_status rs_mvn(rs_stream *stream, const double *L, const double *mean, int64_t
 rs_status rs_mvn_apply(const double *L, const double *mean, int64_t d, uint64_t n, int32_t layout,
                        const double *z_device, double *out, void *cuda_stream);
 
+/* The contraction for a block of `rows` samples, asynchronous and stream-ordered (no host
+ * synchronisation), device pointers only: out = mean + z @ L^T for z rows x d row-major
+ * (continuous.py:332-336 for those rows). layout 0: out is rows x d row-major; layout 1
+ * ("d_n"): out points at column 0 of this block inside a d x ld_out row-major matrix
+ * (ld_out = the whole fill's n). `lower` != 0 asserts that L is lower triangular (exact
+ * zeros above the diagonal; the kernel then skips those products). The Python Rng.mvn
+ * uses it with L and mean uploaded once; a caller may also split a large fill by rows. */
+rs_status rs_mvn_apply_rows(const double *L_device, const double *mean_device, int64_t d, int32_t lower,
+                            uint64_t rows, const double *z_device, int32_t layout, double *out_device,
+                            int64_t ld_out, void *cuda_stream);
+
 /* ---- multi-GPU sharding of variable-consumption fills ----
  * Replaces nothing one-for-one in the reference: it is the rank-local half of
  * `Rng.fill(dist, params, n)` (rng.py:223-241) when one logical stream is split

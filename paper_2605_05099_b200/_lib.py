@@ -111,6 +111,11 @@ def _load():
     L.rs_mvn_apply.argtypes = [ctypes.c_void_p, DBLP, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32,
                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     L.rs_mvn_apply.restype = ctypes.c_int
+    if hasattr(L, "rs_mvn_apply_rows"):  # (absent from older builds used in A/B timing)
+        L.rs_mvn_apply_rows.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                        ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
+                                        ctypes.c_int64, ctypes.c_void_p]
+        L.rs_mvn_apply_rows.restype = ctypes.c_int
     L.rs_dist_info.argtypes = [ctypes.c_int32, DBLP, U64P, ctypes.POINTER(RsDistInfo)]
     L.rs_range_geometry.argtypes = [ctypes.c_int32, ctypes.c_int32, DBLP, U64P, ctypes.c_uint64, U64P,
                                     ctypes.POINTER(ctypes.c_uint32)]
@@ -136,7 +141,7 @@ EXPORTED = (
     "rs_abi_version", "rs_last_error", "rs_init_device", "rs_engine_supported", "rs_engine_state_words",
     "rs_engine_seed_words", "rs_engine_chunk", "rs_seed_words", "rs_engine_seed", "rs_engine_seed_from",
     "rs_engine_check_state", "rs_engine_generate", "rs_engine_jump", "rs_engine_advance_words", "rs_pcg_advance",
-    "rs_fill", "rs_fill_async", "rs_fill_streams", "rs_mvn", "rs_mvn_apply",
+    "rs_fill", "rs_fill_async", "rs_fill_streams", "rs_mvn", "rs_mvn_apply", "rs_mvn_apply_rows",
     "rs_dist_info", "rs_range_geometry", "rs_range_count", "rs_range_count_warm", "rs_range_emit",
 )
 

@@ -57,11 +57,12 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 }
 
 // V: doubles per cp.async (2 when d is even and the pointers 16-byte aligned, else 1).
-// LAYOUT 0: X is n x d row-major (n_d); 1: X^T, d x n row-major (d_n).
+// LAYOUT 0: X is n x d row-major (n_d); 1: X^T, d x ldx row-major (d_n: a block of n rows
+// of a larger fill writes columns [0, n) of rows of length ldx).
 template <int V, int LAYOUT>
 __global__ void __launch_bounds__(MV_THREADS, 2) k_mvn_dmma(const double *__restrict__ z, const double *__restrict__ L,
                                                            const double *__restrict__ mean, double *__restrict__ X,
-                                                           long long n, int d, int lower, int ntn) {
+                                                           long long n, int d, int lower, int ntn, long long ldx) {
     extern __shared__ __align__(128) double mv_smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -166,8 +167,8 @@ __global__ void __launch_bounds__(MV_THREADS, 2) k_mvn_dmma(const double *__rest
                     if (two) p[1] = x1;
                 }
             } else {
-                X[(long long)col * n + row] = x0;
-                if (two) X[(long long)(col + 1) * n + row] = x1;
+                X[(long long)col * ldx + row] = x0;
+                if (two) X[(long long)(col + 1) * ldx + row] = x1;
             }
         }
     }

@@ -946,6 +946,36 @@ RS_DEV bool exp_feed(ZigWM &m, u64 w, ZigFast f, const ZigCtx &z, Tally &t, doub
     return exp_rare(m, w, z, t, out);
 }
 
+// The wedge decision alone (accept / reject) of a token whose first word gave (idx, rabs)
+// and whose second word is w2: state 1 of norm_rare / exp_rare without the output (the
+// batch parse computes the sample value ahead, from the first word).
+RS_DEV bool norm_wedge(u32 idx, u64 rabs, u64 w2, const ZigCtx &z, Tally &t) {
+    u64 yv = w2 >> 12;
+    u64 K = __ldg(&z.slow->k[idx]);
+    u64 lo, hi;
+    zig_lhs(yv, (1ULL << 52) - K, rabs - K, lo, hi);
+    if (lt128(lo, hi, __ldg(&z.slow->ta_lo[idx]), __ldg(&z.slow->ta_hi[idx]))) return true;
+    if (lt128(__ldg(&z.slow->tr_lo[idx]), __ldg(&z.slow->tr_hi[idx]), lo, hi)) return false;
+    t.norm_pdf++;
+    double x = (double)rabs * z.fast[idx].w;
+    double fi = __ldg(&z.slow->f[idx]), fim1 = __ldg(&z.slow->f[idx - 1]);
+    double y = fi + ((double)yv * 2.220446049250313e-16) * (fim1 - fi);
+    return y < det_exp_dev(-0.5 * x * x);
+}
+RS_DEV bool exp_wedge(u32 idx, u64 rabs, u64 w2, const ZigCtx &z, Tally &t) {
+    u64 yv = w2 >> 12;
+    u64 K = __ldg(&z.slow->k[idx]);
+    u64 lo, hi;
+    zig_lhs(yv, (1ULL << 53) - K, rabs - K, lo, hi);
+    if (lt128(lo, hi, __ldg(&z.slow->ta_lo[idx]), __ldg(&z.slow->ta_hi[idx]))) return true;
+    if (lt128(__ldg(&z.slow->tr_lo[idx]), __ldg(&z.slow->tr_hi[idx]), lo, hi)) return false;
+    t.exp_pdf++;
+    double x = (double)rabs * z.fast[idx].w;
+    double fe = __ldg(&z.slow->f[idx]), fem1 = __ldg(&z.slow->f[idx - 1]);
+    double y = fe + ((double)yv * 2.220446049250313e-16) * (fem1 - fe);
+    return y < det_exp_dev(-x);
+}
+
 // ----------------------------------------------------------------------------- distributions
 // A Dist draws one sample per call to sample(s, t). Families share a kernel and pick
 // the law with a (warp-uniform) kind, which keeps the number of kernel instantiations
@@ -968,6 +998,28 @@ struct DistNorm {  // continuous.py:157-158 (norm), :176-177 (lognormal), :281-2
     }
     RS_DEV ZigFast strip(u64 w) const { return z.fast[w & 0xFF]; }
     RS_DEV bool feed(ZigWM &m, u64 w, ZigFast f, Tally &t, double &out) const { return norm_feed(m, w, f, z, t, out); }
+    // batch-parse hooks (rs_kernels.cuh zb_*): a word's fast-path test and signed value, the
+    // wedge decision of a token (first word w1 or a carried state, second word w2), the
+    // state carried into the next batch by a token that starts on its last word
+    static RS_DEV u64 zrabs(u64 w) { return (w >> 9) & ((1ULL << 52) - 1); }
+    RS_DEV bool zfast(u64 w, ZigFast f) const { return zrabs(w) < f.k; }
+    RS_DEV double zval(u64 w, ZigFast f) const {
+        double x = (double)zrabs(w) * f.w;
+        return (w >> 8) & 1 ? -x : x;
+    }
+    RS_DEV bool zwedge(u64 w1, u64 w2, Tally &t) const { return norm_wedge((u32)(w1 & 0xFF), zrabs(w1), w2, z, t); }
+    RS_DEV bool zwedge_m(const ZigWM &m, u64 w2, Tally &t) const { return norm_wedge(m.idx, m.rabs, w2, z, t); }
+    RS_DEV double zval_m(const ZigWM &m) const {
+        double x = (double)m.rabs * z.fast[m.idx].w;
+        return m.neg ? -x : x;
+    }
+    RS_DEV void zcarry(ZigWM &m, u64 w) const {
+        m.st = 1;
+        m.idx = (u32)(w & 0xFF);
+        m.rabs = zrabs(w);
+        m.neg = (u32)((w >> 8) & 1);
+    }
+    RS_DEV void zatt(Tally &t, u32 k) const { t.norm_att += k; }
     RS_DEV bool feed(ZigWM &m, u64 w, Tally &t, double &out) const { return norm_feed(m, w, strip(w), z, t, out); }
     template <class S> RS_DEV void skip_second(S &s, Tally &t) const { std_norm(s, z, t); }
     template <class S> RS_DEV double sample(S &s, Tally &t) const {
@@ -1001,6 +1053,18 @@ struct DistExp {  // continuous.py:165-169 (exp), :252-254 (pareto), :257-266 (g
     }
     RS_DEV ZigFast strip(u64 w) const { return z.fast[w & 0xFF]; }
     RS_DEV bool feed(ZigWM &m, u64 w, ZigFast f, Tally &t, double &out) const { return exp_feed(m, w, f, z, t, out); }
+    static RS_DEV u64 zrabs(u64 w) { return (w >> 8) & ((1ULL << 53) - 1); }
+    RS_DEV bool zfast(u64 w, ZigFast f) const { return zrabs(w) < f.k; }
+    RS_DEV double zval(u64 w, ZigFast f) const { return (double)zrabs(w) * f.w; }
+    RS_DEV bool zwedge(u64 w1, u64 w2, Tally &t) const { return exp_wedge((u32)(w1 & 0xFF), zrabs(w1), w2, z, t); }
+    RS_DEV bool zwedge_m(const ZigWM &m, u64 w2, Tally &t) const { return exp_wedge(m.idx, m.rabs, w2, z, t); }
+    RS_DEV double zval_m(const ZigWM &m) const { return (double)m.rabs * z.fast[m.idx].w; }
+    RS_DEV void zcarry(ZigWM &m, u64 w) const {
+        m.st = 1;
+        m.idx = (u32)(w & 0xFF);
+        m.rabs = zrabs(w);
+    }
+    RS_DEV void zatt(Tally &t, u32 k) const { t.exp_att += k; }
     RS_DEV bool feed(ZigWM &m, u64 w, Tally &t, double &out) const { return exp_feed(m, w, strip(w), z, t, out); }
     template <class S> RS_DEV double sample(S &s, Tally &t) const {
         double e = std_exp(s, z, t);
@@ -1325,6 +1389,13 @@ struct BatchRing {
     RS_DEV void put(T v) {
         ring[(int)((rbase + npend) & (2 * G - 1)) * NT] = v;
         npend++;
+    }
+    // scratch in the free slots: slot_at(free_base() + k) is free until k + 1 more puts
+    RS_DEV u32 free_base() const { return rbase + npend; }
+    RS_DEV void advance(u32 k) { npend += k; }  // k elements written at the free slots
+    RS_DEV u64 *slot_at(u32 i) const {
+        static_assert(sizeof(T) == 8, "8-byte slots");
+        return (u64 *)&ring[(int)(i & (2 * G - 1)) * NT];
     }
     RS_DEV void tick() {
         if (npend < (u32)G) return;

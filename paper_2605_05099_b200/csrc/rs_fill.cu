@@ -1156,6 +1156,33 @@ rs_status rs_fill_streams(int32_t engine, const uint64_t *seed, int32_t n_seed, 
 // rs_mvn (zext == nullptr: z drawn here from `s`) and rs_mvn_apply (z given, on the device).
 // One lock from the scratch sizing to the final synchronisation: the per-device scratch
 // (z, the factor, the mean, the staging buffer) is shared by every caller on the device.
+// One launch of the contraction for `rows` samples: X = mean + z L^T, z rows x d
+// (row-major), X rows x d (layout 0) or columns [0, rows) of a d x ldx matrix (layout 1).
+static rs_status mvn_contract(const double *z, const double *Ld, const double *md, double *X, u64 rows, int64_t d,
+                              int32_t layout, long long ldx, int lower, cudaStream_t st) {
+    // 16-byte copies need an even d (rows 16-byte aligned) and aligned bases
+    const bool vec16 = d % 2 == 0 && (((uintptr_t)z | (uintptr_t)Ld | (uintptr_t)X) & 15) == 0;
+    rsk::MvnLaunch ml = rsk::mvn_kernel(vec16 ? 1 : 0, layout);
+    CK(cudaFuncSetAttribute(ml.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ml.smem));
+    long long nn = (long long)rows;
+    int dd = (int)d;
+    int ntn = (dd + ml.bn - 1) / ml.bn;
+    unsigned long long blocks = (unsigned long long)((rows + ml.bm - 1) / ml.bm) * (unsigned long long)ntn;
+    if (blocks > 0x7FFFFFFFULL) { rs::set_error("mvn too large for one launch"); return RS_ERR_VALUE; }
+    void *args[] = {&z, &Ld, &md, &X, &nn, &dd, &lower, &ntn, &ldx};
+    return launch(ml.fn, dim3((unsigned)blocks), dim3(ml.threads), args, st, ml.smem);
+}
+
+// A Cholesky factor is lower triangular (exact zeros above the diagonal): the kernel
+// skips the zero products. The pivoted semidefinite factor (continuous.py:293-309) is
+// not, and takes the full product.
+static int host_lower(const double *Lh, int64_t d) {
+    for (int64_t r = 0; r < d; r++)
+        for (int64_t q = r + 1; q < d; q++)
+            if (Lh[r * d + q] != 0.0) return 0;
+    return 1;
+}
+
 static rs_status mvn_core(rs_stream *s, const double *L, const double *mean, int64_t d, uint64_t n, int32_t layout,
                           const double *zext, double *out, rs_fill_result *result, void *cuda_stream) {
     if (d < 1 || n < 1) { rs::set_error("mvn needs n >= 1"); return RS_ERR_VALUE; }
@@ -1190,12 +1217,17 @@ static rs_status mvn_core(rs_stream *s, const double *L, const double *mean, int
         c->mvn_bytes = need;
     }
     double *zbuf = c->mvn_z, *Ld = (double *)((char *)c->mvn_z + zb), *md = (double *)((char *)c->mvn_z + zb + lb);
-    const double *z = zext ? zext : zbuf;
+    int lower;
+    if (is_device_ptr(L)) {
+        std::vector<double> hl((size_t)d * d);
+        CK(cudaMemcpyAsync(hl.data(), L, (size_t)d * d * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        lower = host_lower(hl.data(), d);
+    } else {
+        lower = host_lower(L, d);
+    }
     CK(cudaMemcpyAsync(Ld, L, (size_t)d * d * 8, cudaMemcpyDefault, st));
     CK(cudaMemcpyAsync(md, mean, (size_t)d * 8, cudaMemcpyDefault, st));
-    rs_fill_result fr;
-    memset(&fr, 0, sizeof fr);
-    if (!zext && (rc = fill_locked(s, RS_DIST_STDNORM, nullptr, nullptr, nz, zbuf, &fr, cuda_stream))) return rc;
     const bool host_out = !is_device_ptr(out);
     double *X;
     if (host_out) {
@@ -1210,37 +1242,13 @@ static rs_status mvn_core(rs_stream *s, const double *L, const double *mean, int
     } else {
         X = out;
     }
-    // A Cholesky factor is lower triangular (exact zeros above the diagonal): the kernel
-    // skips the zero products. The pivoted semidefinite factor (continuous.py:293-309) is
-    // not, and takes the full product.
-    int lower = 1;
-    {
-        std::vector<double> hl;
-        const double *Lh = L;
-        if (is_device_ptr(L)) {
-            hl.resize((size_t)d * d);
-            CK(cudaMemcpyAsync(hl.data(), L, (size_t)d * d * 8, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            Lh = hl.data();
-        }
-        for (int64_t r = 0; r < d && lower; r++)
-            for (int64_t q = r + 1; q < d; q++)
-                if (Lh[r * d + q] != 0.0) { lower = 0; break; }
-    }
-    // 16-byte copies need an even d (rows 16-byte aligned) and aligned bases
-    const bool vec16 = d % 2 == 0 && (((uintptr_t)z | (uintptr_t)Ld | (uintptr_t)X) & 15) == 0;
-    rsk::MvnLaunch ml = rsk::mvn_kernel(vec16 ? 1 : 0, layout);
-    CK(cudaFuncSetAttribute(ml.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ml.smem));
-    {
-        long long nn = (long long)n;
-        int dd = (int)d;
-        int ntn = (dd + ml.bn - 1) / ml.bn;
-        unsigned long long blocks = (unsigned long long)((n + ml.bm - 1) / ml.bm) * (unsigned long long)ntn;
-        if (blocks > 0x7FFFFFFFULL) { rs::set_error("mvn too large for one launch"); return RS_ERR_VALUE; }
-        const double *zp = z, *lp = Ld, *mp = md;
-        void *args[] = {&zp, &lp, &mp, &X, &nn, &dd, &lower, &ntn};
-        if ((rc = launch(ml.fn, dim3((unsigned)blocks), dim3(ml.threads), args, st, ml.smem))) return rc;
-    }
+    rs_fill_result fr;
+    memset(&fr, 0, sizeof fr);
+    // (A z fill does not overlap the contraction: at 2 blocks/SM the contraction holds the
+    // whole register file, so no parse block can be co-resident; measured with
+    // tools/mvn_overlap.py, the two on separate streams take the sum of their times.)
+    if (!zext && (rc = fill_locked(s, RS_DIST_STDNORM, nullptr, nullptr, nz, zbuf, &fr, cuda_stream))) return rc;
+    if ((rc = mvn_contract(zext ? zext : zbuf, Ld, md, X, n, d, layout, (long long)n, lower, st))) return rc;
     if (host_out) CK(cudaMemcpyAsync(out, X, nz * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
@@ -1257,6 +1265,31 @@ rs_status rs_mvn(rs_stream *s, const double *L, const double *mean, int64_t d, u
 rs_status rs_mvn_apply(const double *L, const double *mean, int64_t d, uint64_t n, int32_t layout,
                        const double *z_device, double *out, void *cuda_stream) {
     return mvn_core(nullptr, L, mean, d, n, layout, z_device, out, nullptr, cuda_stream);
+}
+
+rs_status rs_mvn_apply_rows(const double *L_device, const double *mean_device, int64_t d, int32_t lower,
+                            uint64_t rows, const double *z_device, int32_t layout, double *out_device,
+                            int64_t ld_out, void *cuda_stream) {
+    if (d < 1 || d > (1 << 20)) { rs::set_error("mvn dimension out of range"); return RS_ERR_VALUE; }
+    if (layout != 0 && layout != 1) { rs::set_error("mvn layout must be 'n_d' or 'd_n'"); return RS_ERR_VALUE; }
+    if (rows == 0) { rs::clear_error(); return RS_OK; }
+    if (!is_device_ptr(L_device) || !is_device_ptr(mean_device) || !is_device_ptr(z_device) ||
+        !is_device_ptr(out_device)) {
+        rs::set_error("rs_mvn_apply_rows takes device pointers");
+        return RS_ERR_VALUE;
+    }
+    if (layout == 1 && ld_out < (int64_t)rows) { rs::set_error("mvn ld_out < rows"); return RS_ERR_VALUE; }
+    DeviceGuard dg;
+    cudaPointerAttributes a;
+    CK(cudaPointerGetAttributes(&a, out_device));
+    CK(cudaSetDevice(a.device));
+    rs_status rc = mvn_contract(z_device, L_device, mean_device, out_device, rows, d, layout,
+                                layout == 1 ? (long long)ld_out : (long long)rows, lower ? 1 : 0,
+                                (cudaStream_t)cuda_stream);
+    if (rc) return rc;
+    CK(cudaGetLastError());
+    rs::clear_error();
+    return RS_OK;
 }
 
 // ----------------------------------------------------------------------------- sharded fills

@@ -443,12 +443,74 @@ constexpr int minb(int E, int D) {
 }
 
 // ----------------------------------------------------------------------------- word-level drivers
-// Samples that start before `end` (count) / the next `kmax` samples (emit) with one
-// word per lane per step. The buffered prefix (thread 0 of the first chunk only) is
-// consumed in a preamble so the steady-state loop reads the engine directly and
-// tracks its position with 32-bit counters.
+// Samples that start before `end` (count) / the next `kmax` samples (emit). The buffered
+// prefix (thread 0 of the first chunk only) is consumed in a preamble so the steady-state
+// loop reads the engine directly and tracks its position with 32-bit counters.
+//
+// Batch parse (the bulk of both passes): every lane takes ZB = 8 words per step. The 8
+// fast-path tests and sample values are computed unconditionally (no branch per word);
+// a lane whose 8 words are all fast-path samples from a boundary emits them as they are.
+// Otherwise the lane walks only its non-fast words: a non-fast start is a wedge token
+// (two words, the second one's decision made after the walk) or a tail (the lane then
+// runs the exact word machine over the batch, ~0.2 % of lane-batches). The wedge
+// consumption is 2 words whatever the decision, so the token structure is known before
+// any decision is made, and the decisions of a batch run once per warp for all lanes
+// (the per-word machine ran its rare branch on ~37 % of warp-steps, one lane active).
+// An accepted wedge's sample takes its first word's slot, so samples stay in order.
+constexpr int ZB = 8;
+
+// The batch's token structure in machine state m (0, or 1 = a wedge carried from the
+// previous batch whose second word is w[0]). Returns false when the lane must take the
+// exact machine (a carried tail, or a tail token in the batch) -- before any side effect.
+// Otherwise: O = sample slots (fast starts, accepted wedges at their first word, and bit 0
+// for an accepted carried wedge, whose value is xc), att = attempts started in the batch,
+// m = the state carried out (1: a wedge starts on the last word), bnd = the batch ends on
+// a sample boundary.
+// WS: the batch's words staged in shared memory, ws(q) = word q. F: fast-path bits, Z: bits
+// of words whose strip index is 0 (a non-fast start there is a tail).
+template <class D, class WS>
+__device__ __forceinline__ bool zb_tokens(const D &d, ZigWM &m, const WS &ws, u32 F, u32 Z, u32 &O, u32 &att,
+                                       bool &bnd, double &xc, Tally &tl) {
+    const u32 cin = m.st;
+    const u32 N = ~F & 0xFFu;
+    // (a non-fast word with index 0 may be a tail start: the exact machine takes the batch;
+    // ~0.2 % of lane-batches, some of them a wedge's second word that only looks like one)
+    if (cin >= 2 || (N & Z)) return false;
+    u32 Wm, starts = cin ? 0xFEu : 0xFFu;
+    if ((N & (N >> 1)) == 0) {  // no two non-fast words in a row: each one (but a carried
+        Wm = N & starts;        // wedge's second word) starts a wedge
+    } else {
+        Wm = 0;
+        u32 cand = N & starts;
+        while (cand) {
+            const int q = __ffs(cand) - 1;
+            Wm |= 1u << q;
+            starts &= ~(2u << q);  // the next word is the wedge's second
+            cand = N & starts & ~((2u << q) - 1u);
+        }
+    }
+    starts &= ~(Wm << 1);
+    u32 o = F & starts;
+    if (cin) {
+        xc = d.zval_m(m);
+        if (d.zwedge_m(m, ws(0), tl)) o |= 1u;
+    }
+    u32 dw = Wm & 0x7Fu;
+    while (dw) {
+        const int q = __ffs(dw) - 1;
+        dw &= dw - 1;
+        if (d.zwedge(ws(q), ws(q + 1), tl)) o |= 1u << q;
+    }
+    if (Wm & 0x80u) d.zcarry(m, ws(ZB - 1));
+    else m.st = 0;
+    bnd = ((o >> 7) & 1) || (((Wm >> 6) & 1) && ((o >> 6) & 1));
+    O = o;
+    att = __popc(starts);
+    return true;
+}
+
 template <class D, class SRC>
-__device__ __forceinline__ u64 wl_count(const D &d, SRC &s, u64 end, Tally &tl) {
+__device__ __forceinline__ u64 wl_count(const D &d, SRC &s, u64 end, Tally &tl, u64 *wsm) {
     ZigWM m;
     m.st = 0;
     bool bnd = true;
@@ -459,29 +521,46 @@ __device__ __forceinline__ u64 wl_count(const D &d, SRC &s, u64 end, Tally &tl) 
         c += bnd;
     }
     u32 left = s.pos < end ? (u32)(end - s.pos) : 0u, used = 0, cc = 0;
-    // 4 words per step: the engine chain and the 4 strip loads overlap. While a whole
-    // batch lies inside the segment no exit is possible, so the bulk loop tests nothing
-    // per word; the tail loop below stops at the first boundary past the end (words
-    // generated past the exit are dropped: only the position matters).
-    if (bnd) {
-        u32 b = 1;
-        while (used + 4 <= left) {
-            u64 w[4];
+    // batches that lie inside the segment (no exit is possible inside them)
+    auto ws = [wsm](int q) -> u64 { return wsm[q * BLOCK]; };
+    while (used + ZB <= left) {
+        u64 w[ZB];
+#pragma unroll
+        for (int k = 0; k < ZB; k++) w[k] = s.e.next();
+        u32 F = 0, Z = 0;
+#pragma unroll
+        for (int h = 0; h < ZB; h += 4) {
             ZigFast f[4];
 #pragma unroll
-            for (int k = 0; k < 4; k++) w[k] = s.e.next();
-#pragma unroll
-            for (int k = 0; k < 4; k++) f[k] = d.strip(w[k]);
+            for (int k = 0; k < 4; k++) f[k] = d.strip(w[h + k]);
 #pragma unroll
             for (int k = 0; k < 4; k++) {
-                double z;
-                b = d.feed(m, w[k], f[k], tl, z) ? 1u : 0u;
-                cc += b;
+                F |= (d.zfast(w[h + k], f[k]) ? 1u : 0u) << (h + k);
+                Z |= ((w[h + k] & 0xFF) == 0 ? 1u : 0u) << (h + k);
             }
-            used += 4;
         }
-        bnd = b != 0;
+        if (F == 0xFFu && m.st == 0) {
+            cc += ZB;
+            bnd = true;
+        } else {
+#pragma unroll
+            for (int k = 0; k < ZB; k++) wsm[k * BLOCK] = w[k];
+            u32 O, att;
+            double xc;
+            if (zb_tokens(d, m, ws, F, Z, O, att, bnd, xc, tl)) {
+                cc += __popc(O);
+            } else {  // exact machine over the batch
+                for (int k = 0; k < ZB; k++) {
+                    double z;
+                    bnd = d.feed(m, ws(k), tl, z);
+                    cc += bnd;
+                }
+            }
+        }
+        used += ZB;
     }
+    // the rest of the segment word by word, up to the first boundary past its end (words
+    // generated past the exit are dropped: only the position matters)
     while (!(bnd && used >= left)) {
         u64 w[4];
         ZigFast f[4];
@@ -503,6 +582,7 @@ __device__ __forceinline__ u64 wl_count(const D &d, SRC &s, u64 end, Tally &tl) 
 }
 template <class D, class SRC, class W>
 __device__ __forceinline__ void wl_emit(const D &d, SRC &s, u64 kmax, W &wr, Tally &tl) {
+    static_assert(W::G == ZB, "one BatchRing group per batch");
     ZigWM m;
     m.st = 0;
     u64 k = 0;
@@ -512,9 +592,72 @@ __device__ __forceinline__ void wl_emit(const D &d, SRC &s, u64 kmax, W &wr, Tal
         wr.tick();  // (thread 0 only: one sample per tick keeps the ring bound)
     }
     u32 left = (u32)(kmax - k), used = 0;
-    // one word of software pipelining: the next word is generated and its strip load
-    // issued before the current word is fed (the extra word at the end is never fed;
-    // the position counts fed words only)
+    // batches while at least ZB samples remain (a batch emits at most ZB). A slow batch
+    // stages its words in the ring's free slots (at most G - 1 samples are pending after a
+    // tick, so the next ZB slots are free; the batch's own samples overwrite them in order,
+    // after the words have been read).
+    while (left >= ZB) {
+        u64 w[ZB];
+#pragma unroll
+        for (int q = 0; q < ZB; q++) w[q] = s.e.next();
+        u32 F = 0, Z = 0;
+        double x[ZB];
+#pragma unroll
+        for (int h = 0; h < ZB; h += 4) {
+            ZigFast f[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) f[q] = d.strip(w[h + q]);
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                F |= (d.zfast(w[h + q], f[q]) ? 1u : 0u) << (h + q);
+                Z |= ((w[h + q] & 0xFF) == 0 ? 1u : 0u) << (h + q);
+                x[h + q] = d.zval(w[h + q], f[q]);
+            }
+        }
+        u32 O = 0xFFu;
+        if (F != 0xFFu || m.st != 0) {
+            const u32 fb = wr.free_base();
+#pragma unroll
+            for (int q = 0; q < ZB; q++) *wr.slot_at(fb + q) = w[q];
+            auto ws = [&wr, fb](int q) -> u64 { return *wr.slot_at(fb + (u32)q); };
+            u32 att;
+            bool bnd;
+            double xc = 0.0;
+            const u32 cin = m.st;
+            if (zb_tokens(d, m, ws, F, Z, O, att, bnd, xc, tl)) {
+                d.zatt(tl, att);
+                if (cin) x[0] = xc;  // the carried wedge's sample takes slot 0 (its second word)
+            } else {  // exact machine over the batch, writing its own samples
+                // (the j-th put of the batch lands in staged slot j <= the word being fed)
+                O = 0;
+                for (int q = 0; q < ZB; q++) {
+                    double z;
+                    if (d.feed(m, ws(q), tl, z)) { wr.put(d.finish(z)); left--; }
+                }
+            }
+        } else {
+            d.zatt(tl, ZB);
+        }
+        // the batch's samples into the ring without a branch per word: x[q] goes to the slot
+        // after the samples of the words before it, so a word without a sample is overwritten
+        // by the next sample (or lands in a free slot past them)
+        {
+            const u32 fb = wr.free_base();
+            u32 c = 0;
+#pragma unroll
+            for (int q = 0; q < ZB; q++) {
+                *(double *)wr.slot_at(fb + c) = d.finish(x[q]);
+                c += (O >> q) & 1;
+            }
+            wr.advance(c);
+        }
+        left -= __popc(O);
+        used += ZB;
+        wr.tick();
+    }
+    // the last < ZB samples word by word (one word of software pipelining: the next word is
+    // generated and its strip load issued before the current word is fed; the extra word
+    // at the end is never fed, the position counts fed words only)
     u64 wn = s.e.next();
     ZigFast fn = d.strip(wn);
     while (left) {
@@ -525,7 +668,7 @@ __device__ __forceinline__ void wl_emit(const D &d, SRC &s, u64 kmax, W &wr, Tal
         double z;
         used++;
         if (d.feed(m, w, f, tl, z)) { wr.put(d.finish(z)); left--; }
-        if ((used & (W::G - 1)) == 0) wr.tick();  // the same steps in every lane of the warp
+        if ((used & (W::G - 1)) == 0) wr.tick();
     }
     s.pos += used;
 }
@@ -671,6 +814,7 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_count(const __grid_consta
                                                             u64 *cnt1, u32 *ex1) {
     __shared__ ZigFast sm[256];
     __shared__ __align__(16) unsigned char ring_sp[D == FAM_GAMMA ? 128 * BLOCK : 16];  // speculative store
+    __shared__ u64 zb_sm[(D == FAM_NORM || D == FAM_EXP) ? ZB * BLOCK : 1];              // batch words
     stage_tables(p, sm);
     u32 t = blockIdx.x * BLOCK + threadIdx.x;
     if (t >= p.T) return;
@@ -693,7 +837,7 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_count(const __grid_consta
         bool done = false;
         if constexpr (D == FAM_NORM || D == FAM_EXP) {
             if (d.word_level()) {  // one word per lane per step (uniform engine step)
-                c = wl_count(d, s, end, tl);
+                c = wl_count(d, s, end, tl, zb_sm + threadIdx.x);
                 done = true;
             }
         }

@@ -505,40 +505,61 @@ class Rng:
     @_op
     def mvn(self, mean, cov, n=1, layout="n_d"):
         """continuous.py:312-336: X = mean + z @ L^T, z = n*d std_norm draws (row-major),
-        L = Cholesky factor (pivoted LAPACK fallback for semidefinite S)."""
+        L = Cholesky factor (pivoted LAPACK fallback for semidefinite S).
+
+        The host checks symmetry and factorises S on a worker thread while the device draws z
+        (numpy and LAPACK release the GIL, and so does the ctypes fill); the contraction
+        (rs_mvn_apply_rows) is queued on the current stream once the factor is ready."""
         mean = np.asarray(mean, dtype=np.float64)
         cov = np.asarray(cov, dtype=np.float64)
         if mean.ndim != 1 or cov.shape != (mean.size, mean.size):
             raise ValueError("mvn needs a length-d mean and a d x d covariance")
-        if not np.allclose(cov, cov.T, rtol=1e-9, atol=1e-12):
-            raise ValueError("mvn covariance must be symmetric")
+
+        def symmetric():
+            if not np.allclose(cov, cov.T, rtol=1e-9, atol=1e-12):
+                raise ValueError("mvn covariance must be symmetric")
+
+        # the reference's error order: symmetry, layout, n (an earlier error wins)
         if layout not in ("n_d", "d_n"):
+            symmetric()
             raise ValueError("mvn layout must be 'n_d' or 'd_n'")
-        n = int(n)
+        try:
+            n = int(n)
+        except Exception:
+            symmetric()
+            raise
         if n < 1:
+            symmetric()
             raise ValueError("mvn needs n >= 1")
         d = mean.size
         dev = self._device()
+
+        def factorise():
+            symmetric()
+            f = np.ascontiguousarray(semidefinite_factor(cov))
+            return f, not np.triu(f, 1).any()
+
         out = torch.empty((n, d) if layout == "n_d" else (d, n), dtype=torch.float64, device=dev)
         z = torch.empty(n * d, dtype=torch.float64, device=dev)
-        # The host factorises S while the device draws z (both release the GIL). The
-        # reference factorises first (continuous.py:312-336), so a failed factorisation
-        # puts the generator back where it was: nothing observable is consumed.
+        # The reference factorises before drawing (continuous.py:331), so a failed
+        # factorisation puts the generator back where it was: nothing observable is consumed.
         before = (list(self.engine.s), self.buffer.capture(), {k: dict(v) for k, v in self.counters.items()})
-        fut = _host_pool().submit(semidefinite_factor, cov)
+        fut = _host_pool().submit(factorise)
         try:
             self.device_fill("stdnorm", [], [], n * d, out=z)
         finally:
             try:
-                factor = np.ascontiguousarray(fut.result())
+                factor, lower = fut.result()
             except Exception:
                 self.engine.s, self.counters = before[0], before[2]
                 self.buffer.restore(before[1])
                 raise
-        mptr = np.ascontiguousarray(mean)
-        _lib.check(_lib.lib.rs_mvn_apply(ctypes.c_void_p(factor.ctypes.data), mptr.ctypes.data_as(_lib.DBLP), d, n,
-                                         0 if layout == "n_d" else 1, ctypes.c_void_p(z.data_ptr()),
-                                         ctypes.c_void_p(out.data_ptr()), _cuda_stream_ptr(dev)))
+        Ld = torch.from_numpy(factor).to(dev)
+        md = torch.from_numpy(np.ascontiguousarray(mean)).to(dev)
+        _lib.check(_lib.lib.rs_mvn_apply_rows(
+            ctypes.c_void_p(Ld.data_ptr()), ctypes.c_void_p(md.data_ptr()), d, 1 if lower else 0, n,
+            ctypes.c_void_p(z.data_ptr()), 0 if layout == "n_d" else 1, ctypes.c_void_p(out.data_ptr()), n,
+            _cuda_stream_ptr(dev)))
         return out
 
 

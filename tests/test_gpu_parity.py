@@ -748,6 +748,104 @@ def test_mvn_indefinite_covariance_consumes_nothing():
     assert np.array_equal(_bits(got), _bits(ref))
 
 
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("semidef", [False, True])
+def test_mvn_apply_rows_blocks(layout, semidef):
+    """rs_mvn_apply_rows (asynchronous, device pointers) over row blocks of one fill (128 rows
+    and a ragged last block, written into the right rows / columns of X) equals
+    mean + z @ L^T; the pivoted factor takes the full product, the Cholesky one the
+    triangular one."""
+    import ctypes
+    from paper_2605_05099_b200 import _lib
+    from paper_2605_05099_b200.rng import semidefinite_factor
+    d, n = 24, 128 * 7 + 45
+    g = np.random.default_rng(11)
+    B = g.standard_normal((d, 5 if semidef else d))
+    S = B @ B.T / d + (0.0 if semidef else 1.0) * np.eye(d)
+    Lf = semidefinite_factor(S)
+    lower = not np.triu(Lf, 1).any()
+    assert lower != semidef
+    mean = np.linspace(-2, 2, d)
+    z = g.standard_normal((n, d))
+    zd = torch.from_numpy(z).cuda()
+    Ld = torch.from_numpy(np.ascontiguousarray(Lf)).cuda()
+    md = torch.from_numpy(mean).cuda()
+    X = torch.full((n, d) if layout == 0 else (d, n), np.nan, dtype=torch.float64, device="cuda")
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for r0 in range(0, n, 128):
+        rows = min(128, n - r0)
+        o = X.data_ptr() + 8 * (r0 * d if layout == 0 else r0)
+        _lib.check(_lib.lib.rs_mvn_apply_rows(ctypes.c_void_p(Ld.data_ptr()), ctypes.c_void_p(md.data_ptr()), d,
+                                              1 if lower else 0, rows, ctypes.c_void_p(zd.data_ptr() + 8 * r0 * d),
+                                              layout, ctypes.c_void_p(o), n, st))
+    Xh = X.cpu().numpy()
+    if layout == 1:
+        Xh = Xh.T
+    ref = mean + z @ Lf.T
+    scale = np.abs(z) @ np.abs(Lf).T + np.abs(mean)
+    assert np.max(np.abs(Xh - ref) / scale) <= 1e-12
+
+
+def test_mvn_error_order():
+    """The reference's validation order (continuous.py:319-329): shape, symmetry, layout, n."""
+    r = state_io.create("philox", seed=[3])
+    before = _state_of(r)
+    asym = np.array([[1.0, 0.5], [0.0, 1.0]])
+    with pytest.raises(ValueError, match="symmetric"):
+        r.mvn(np.zeros(2), asym, n=10, layout="bad")
+    with pytest.raises(ValueError, match="symmetric"):
+        r.mvn(np.zeros(2), asym, n=0)
+    with pytest.raises(ValueError, match="symmetric"):
+        r.mvn(np.zeros(2), asym, n=10)
+    with pytest.raises(ValueError, match="layout"):
+        r.mvn(np.zeros(2), np.eye(2), n=10, layout="bad")
+    with pytest.raises(ValueError, match="n >= 1"):
+        r.mvn(np.zeros(2), np.eye(2), n=0)
+    assert _state_of(r) == before
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+def test_rs_mvn_c_abi(layout):
+    """rs_mvn (the C entry point, include/randstream_b200.h) draws z itself and contracts it:
+    d = 64, n = 2^16 + 77 from a mid-buffer pcg64 stream, against the oracle's z @ L^T, its
+    final position and its tallies."""
+    import ctypes
+    from paper_2605_05099_b200 import _lib
+    d, n = 64, (1 << 16) + 77
+    g = np.random.default_rng(5)
+    A = g.standard_normal((d, d))
+    S = A @ A.T / d + np.eye(d)
+    L = np.ascontiguousarray(np.linalg.cholesky(S))
+    mean = np.linspace(0, 1, d)
+    r = state_io.create("pcg64", seed=[23])
+    o = O.OracleRng("pcg64", seed=[23])
+    for _ in range(5):
+        r.next_u64()
+        o.next_u64()
+    X = torch.empty((n, d) if layout == 0 else (d, n), dtype=torch.float64, device="cuda")
+    st = r.to_stream()
+    res = _lib.RsFillResult()
+    _lib.check(_lib.lib.rs_mvn(ctypes.byref(st), ctypes.c_void_p(L.ctypes.data), mean.ctypes.data_as(_lib.DBLP), d, n,
+                               layout, ctypes.c_void_p(X.data_ptr()), ctypes.byref(res),
+                               ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    r.from_stream(st)
+    Xh = X.cpu().numpy()
+    if layout == 1:
+        Xh = Xh.T
+    rows = 1 << 16
+    worst = 0.0
+    for a in range(0, n, rows):
+        k = min(rows, n - a)
+        z = o.fill("stdnorm", {}, k * d).reshape(k, d)
+        ref = mean + z @ L.T
+        scale = np.abs(z) @ np.abs(L).T + np.abs(mean)
+        worst = max(worst, float(np.max(np.abs(Xh[a:a + k] - ref) / scale)))
+    assert worst <= 1e-12, worst
+    _assert_same_position(r, o)
+    t = o.tallies()["norm"]
+    assert (res.tally[0], res.tally[1]) == (t["attempts"], t["pdf_evals"])
+
+
 @pytest.mark.parametrize("engine,dist,params", [("x256**", "norm", {}), ("pcg64", "gamma", {"alpha": 2.5}),
                                                 ("philox", "u01f", {}), ("sfc64", "uint64", {"b": 1000003})])
 def test_integration_device_fill(engine, dist, params):

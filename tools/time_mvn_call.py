@@ -30,6 +30,15 @@ r = state_io.create("philox", seed=[31])
 A = r.fill("norm", {}, d * d).cpu().numpy().reshape(d, d)
 S = A @ A.T / d + np.eye(d)
 print("whole r.mvn        %.3f ms" % best(lambda: r.mvn(np.zeros(d), S, n=n)))
+print("sym check (host)   %.3f ms" % best(lambda: np.allclose(S, S.T, rtol=1e-9, atol=1e-12)))
+Ld = torch.from_numpy(np.ascontiguousarray(np.linalg.cholesky(S))).cuda()
+stC = r.to_stream()
+Xc = torch.empty((n, d), dtype=torch.float64, device="cuda")
+mz = np.zeros(d)
+print("rs_mvn (C ABI)      %.3f ms" % best(lambda: _lib.check(_lib.lib.rs_mvn(
+    ctypes.byref(stC), ctypes.c_void_p(Ld.data_ptr()), mz.ctypes.data_as(_lib.DBLP), d, n, 0,
+    ctypes.c_void_p(Xc.data_ptr()), None, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))))
+del Xc
 z = torch.empty(n * d, dtype=torch.float64, device="cuda")
 print("z fill (stdnorm)   %.3f ms" % best(lambda: r.device_fill("stdnorm", [], [], n * d, out=z)))
 print("cholesky (host)    %.3f ms" % best(lambda: semidefinite_factor(S)))
