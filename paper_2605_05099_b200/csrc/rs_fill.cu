@@ -22,7 +22,6 @@
 //   emit   : each thread re-parses from its true entry and writes its samples at
 //            their global offsets.
 // Non-convergence inside a segment is detected and iterated to a fixed point.
-#include <cub/device/device_scan.cuh>
 
 #include "rs_kernels.cuh"
 
@@ -47,12 +46,10 @@ struct DevCtx {
     u64 *rlxA = nullptr;
     // scratch
     size_t cap_T = 0;
-    u64 *states = nullptr, *cnt0 = nullptr, *cnt1 = nullptr, *cnt = nullptr, *off = nullptr;
+    u64 *states = nullptr, *cnt0 = nullptr, *cnt1 = nullptr, *cnt = nullptr, *bsum = nullptr;  // bsum: per-block count sums (k_fixup -> k_emit)
     u32 *ex0 = nullptr, *ex1 = nullptr, *exA = nullptr, *exB = nullptr, *entry = nullptr;
     u32 *bm = nullptr;  // [2][bmw][T] boundary bitmaps
     size_t bm_bytes = 0;
-    void *cub_tmp = nullptr;
-    size_t cub_bytes = 0;
     DevResult *res = nullptr;
     DevResult *res_host = nullptr;
     std::map<std::tuple<int, u64, int>, u64 *> x256_ml;  // (family, L, levels) -> matrices
@@ -129,21 +126,18 @@ rs_status init_dev(int dev, DevCtx **out) {
 rs_status ensure_scratch(DevCtx &c, size_t T) {
     if (T <= c.cap_T) return RS_OK;
     size_t nT = T + T / 4;
-    cudaFree(c.states); cudaFree(c.cnt0); cudaFree(c.cnt1); cudaFree(c.cnt); cudaFree(c.off);
-    cudaFree(c.ex0); cudaFree(c.ex1); cudaFree(c.exA); cudaFree(c.exB); cudaFree(c.entry); cudaFree(c.cub_tmp);
+    cudaFree(c.states); cudaFree(c.cnt0); cudaFree(c.cnt1); cudaFree(c.cnt); cudaFree(c.bsum);
+    cudaFree(c.ex0); cudaFree(c.ex1); cudaFree(c.exA); cudaFree(c.exB); cudaFree(c.entry);
     CK(cudaMalloc(&c.states, nT * 32));
     CK(cudaMalloc(&c.cnt0, nT * 8));
     CK(cudaMalloc(&c.cnt1, nT * 8));
     CK(cudaMalloc(&c.ex1, nT * 4));
     CK(cudaMalloc(&c.cnt, nT * 8));
-    CK(cudaMalloc(&c.off, nT * 8));
+    CK(cudaMalloc(&c.bsum, (nT / BLOCK + 2) * 8));
     CK(cudaMalloc(&c.ex0, nT * 4));
     CK(cudaMalloc(&c.exA, nT * 4));
     CK(cudaMalloc(&c.exB, nT * 4));
     CK(cudaMalloc(&c.entry, nT * 4));
-    c.cub_bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, c.cub_bytes, c.cnt, c.off, (int)nT);
-    CK(cudaMalloc(&c.cub_tmp, c.cub_bytes));
     c.cap_T = nT;
     return RS_OK;
 }
@@ -852,14 +846,13 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
             void *a1[] = {&p, &c.cnt0, &c.ex0, &c.cnt1, &c.ex1};
             if ((rc = launch(K.count, dim3(g), dim3(BLOCK), a1, st))) return rc;
             const u32 *prev = c.ex0;
-            void *a2[] = {&p, &c.cnt0, &c.ex0, &c.cnt1, &c.ex1, &prev, &c.entry, &c.cnt, &c.exA, &round, &res};
+            void *a2[] = {&p, &c.cnt0, &c.ex0, &c.cnt1, &c.ex1, &prev, &c.entry, &c.cnt, &c.exA, &round, &res, &c.bsum};
             if ((rc = launch(K.fixup, dim3(g), dim3(BLOCK), a2, st))) return rc;
         }
         u32 *ex_cur = c.exA, *ex_other = c.exB;
         for (;;) {
-            size_t bytes = c.cub_bytes;
-            CK(cub::DeviceScan::ExclusiveSum(c.cub_tmp, bytes, c.cnt, c.off, (int)p.T, st));
-            void *a3[] = {&p, &c.entry, &c.cnt, &c.off, &ex_cur, &res};
+            // (no scan launch: the fixup left per-block count sums, the emit blocks finish the offsets)
+            void *a3[] = {&p, &c.entry, &c.cnt, &c.bsum, &ex_cur, &res};
             if ((rc = launch(K.emit, dim3(g), dim3(BLOCK), a3, st))) return rc;
             if (!sync) { chunks++; return RS_OK; }
             CK(cudaMemcpyAsync(c.res_host, c.res, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
@@ -871,7 +864,7 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
             rounds++;
             CK(cudaMemsetAsync(c.res, 0, offsetof(DevResult, serial_state), st));
             const u32 *prev = ex_cur;
-            void *a2[] = {&p, &c.cnt0, &c.ex0, &c.cnt1, &c.ex1, &prev, &c.entry, &c.cnt, &ex_other, &round, &res};
+            void *a2[] = {&p, &c.cnt0, &c.ex0, &c.cnt1, &c.ex1, &prev, &c.entry, &c.cnt, &ex_other, &round, &res, &c.bsum};
             if ((rc = launch(K.fixup, dim3(g), dim3(BLOCK), a2, st))) return rc;
             u32 *tmp = ex_cur; ex_cur = ex_other; ex_other = tmp;
         }
@@ -1388,6 +1381,7 @@ static rs_status range_count_core(const rs_stream *s, int32_t dist, const double
     memcpy(p.lanes, s->state, sizeof p.lanes);
     p.lp0 = n_warm ? 0 : entry;
     p.n = 0;
+    p.n_warm = n_warm;
     const u32 Tall = n_warm + n_seg;
     VarKernels K = var_kernels(s->engine, r.family);
     const bool mem = parse_from_memory(s->engine);
@@ -1401,37 +1395,29 @@ static rs_status range_count_core(const rs_stream *s, int32_t dist, const double
     if ((rc = launch(K.count, dim3(gdim), dim3(BLOCK), a1, st))) return rc;
     const u32 *prev = c->ex0;
     u32 *ex_cur = c->exA, *ex_other = c->exB;
-    void *a2[] = {&p, &c->cnt0, &c->ex0, &c->cnt1, &c->ex1, &prev, &c->entry, &c->cnt, &ex_cur, &round, &res};
+    void *a2[] = {&p, &c->cnt0, &c->ex0, &c->cnt1, &c->ex1, &prev, &c->entry, &c->cnt, &ex_cur, &round, &res, &c->bsum};
     if ((rc = launch(K.fixup, dim3(gdim), dim3(BLOCK), a2, st))) return rc;
     int rounds = 0;
+    // The fixup zeroes the warm-up segments' counts and accumulates the slice's total, so
+    // one read-back per round carries everything: the flag, the total, the last exit and
+    // the window's exit (the slice's entry).
+    u32 last_ex = 0, e32 = 0;
     for (;;) {  // entry resolution to a fixed point (as run_fill)
         CK(cudaMemcpyAsync(c->res_host, c->res, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&last_ex, ex_cur + (p.T - 1), 4, cudaMemcpyDeviceToHost, st));
+        if (n_warm) CK(cudaMemcpyAsync(&e32, ex_cur + (n_warm - 1), 4, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         if (!c->res_host->flag) break;
         if (++round > (int)p.T) { rs::set_error("segment entry resolution did not converge"); return RS_ERR_INTERNAL; }
         rounds++;
         CK(cudaMemsetAsync(c->res, 0, offsetof(DevResult, serial_state), st));
         prev = ex_cur;
-        void *a3[] = {&p, &c->cnt0, &c->ex0, &c->cnt1, &c->ex1, &prev, &c->entry, &c->cnt, &ex_other, &round, &res};
+        void *a3[] = {&p, &c->cnt0, &c->ex0, &c->cnt1, &c->ex1, &prev, &c->entry, &c->cnt, &ex_other, &round, &res, &c->bsum};
         if ((rc = launch(K.fixup, dim3(gdim), dim3(BLOCK), a3, st))) return rc;
         u32 *tmp = ex_cur; ex_cur = ex_other; ex_other = tmp;
     }
-    u64 wentry = entry;
-    if (n_warm) {  // the warm-up segments emit nothing; the slice enters at the window's exit
-        CK(cudaMemsetAsync(c->cnt, 0, (size_t)n_warm * 8, st));
-        u32 e32 = 0;
-        CK(cudaMemcpyAsync(&e32, ex_cur + (n_warm - 1), 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        wentry = e32;
-    }
-    size_t bytes = c->cub_bytes;
-    CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, c->cnt, c->off, (int)p.T, st));
-    u64 last_off = 0, last_cnt = 0;
-    u32 last_ex = 0;
-    CK(cudaMemcpyAsync(&last_off, c->off + (p.T - 1), 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&last_cnt, c->cnt + (p.T - 1), 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&last_ex, ex_cur + (p.T - 1), 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    const u64 wentry = n_warm ? (u64)e32 : entry;  // the slice enters at the window's exit
+    const u64 total = c->res_host->total;
     if (mem) {
         u32 over = 0, zero = 0;
         CK(cudaMemcpy(&over, c->overrun, sizeof over, cudaMemcpyDeviceToHost));
@@ -1444,7 +1430,7 @@ static rs_status range_count_core(const rs_stream *s, int32_t dist, const double
     c->range.p = p;
     c->range.K = K;
     c->range.ex = ex_cur;
-    c->range.count = last_off + last_cnt;
+    c->range.count = total;
     c->range.unit = r.unit;
     c->range.mem = mem;
     c->range.origin = u * seg_len * (u64)n_warm;
@@ -1452,7 +1438,7 @@ static rs_status range_count_core(const rs_stream *s, int32_t dist, const double
     c->range.valid = true;
     if (info) {
         memset(info, 0, sizeof *info);
-        info->count = last_off + last_cnt;
+        info->count = total;
         info->exit = last_ex;  // seg_end(T-1) == units(slice): the exit is past the slice end
         info->end_pos = wentry;
         info->unit = r.unit;
@@ -1500,7 +1486,7 @@ rs_status rs_range_emit(uint64_t keep, void *out_device, rs_range_info *info, vo
     p.out0 = 0;
     CK(cudaMemsetAsync(c->res, 0, offsetof(DevResult, serial_state), st));
     DevResult *res = c->res;
-    void *a[] = {&p, &c->entry, &c->cnt, &c->off, &R.ex, &res};
+    void *a[] = {&p, &c->entry, &c->cnt, &c->bsum, &R.ex, &res};
     if ((rc = launch(R.K.emit, dim3(p.T / BLOCK), dim3(BLOCK), a, st))) return rc;
     CK(cudaMemcpyAsync(c->res_host, c->res, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

@@ -88,6 +88,8 @@ struct FillPlan {
     u32 *spec1_tal;               // [T][spec_cap]
     u32 *c1own;                   // phase-1 samples before the merge (all of them if none)
     u32 *mrank0;                  // phase-0 sample index at the merge point
+    // counted ranges: the first n_warm segments only resolve the slice's entry (count 0)
+    u32 n_warm;
 };
 // per-sample tally word of the gamma attempt machine: gamma attempts (8 bits), normal
 // attempts (12), normal pdf evaluations (12); 0xFFFFFFFF never occurs (flagged instead)
@@ -1020,44 +1022,93 @@ __device__ void resolve_entry(const FillPlan &p, const ZigFast *sm, u32 t, u32 e
     }
 }
 
-// round 0: prev_ex = ex0, every thread; round r>0: only threads whose entry changed.
+// Output offsets without a scan launch: k_fixup leaves the sum of each block's counts
+// (bsum[block]) and their total; an emit block adds the sums of the blocks before it
+// (<= T / BLOCK values) to the exclusive scan of its own BLOCK counts.
+__device__ __forceinline__ u64 warp_sum64(u64 v) {
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, sh);
+    return v;
+}
+__device__ __forceinline__ u64 block_offset(const u64 *bsum, u64 c) {
+    __shared__ u64 wtot[BLOCK / 32], wbase[BLOCK / 32];
+    const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    u64 b = 0;
+    for (u32 i = threadIdx.x; i < blockIdx.x; i += BLOCK) b += bsum[i];
+    b = warp_sum64(b);
+    u64 inc = c;
+#pragma unroll
+    for (int sh = 1; sh < 32; sh <<= 1) {
+        u64 v = __shfl_up_sync(0xFFFFFFFFu, inc, sh);
+        if (lane >= (u32)sh) inc += v;
+    }
+    if (lane == 31) wtot[wid] = inc;
+    if (lane == 0) wbase[wid] = b;
+    __syncthreads();
+    u64 o = inc - c;
+#pragma unroll
+    for (int w = 0; w < BLOCK / 32; w++) {
+        o += wbase[w];
+        if ((u32)w < wid) o += wtot[w];
+    }
+    return o;
+}
+
+// round 0: prev_ex = ex0, every thread; round r>0: only threads whose entry changed
+// re-resolve; every thread contributes its count to the block's sum.
 template <int E, int D>
 __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_fixup(const __grid_constant__ FillPlan p, const u64 *cnt0, const u32 *ex0,
                                                  const u64 *cnt1, const u32 *ex1, const u32 *prev_ex, u32 *entry,
-                                                 u64 *cnt, u32 *ex, int round, DevResult *res) {
+                                                 u64 *cnt, u32 *ex, int round, DevResult *res, u64 *bsum) {
     __shared__ ZigFast sm[256];
+    __shared__ u64 wsum[BLOCK / 32];
     stage_tables(p, sm);
     u32 t = blockIdx.x * BLOCK + threadIdx.x;
-    if (t >= p.T) return;
-    u32 e = t == 0 ? 0u : prev_ex[t - 1];
-    if (round > 0 && e == entry[t]) {
-        ex[t] = prev_ex[t];
-        return;
+    u64 c = 0;
+    if (t < p.T) {
+        u32 e = t == 0 ? 0u : prev_ex[t - 1];
+        if (round > 0 && e == entry[t]) {
+            ex[t] = prev_ex[t];
+            c = cnt[t];
+        } else {
+            entry[t] = e;
+            u32 x;
+            if (e == 0) {
+                c = cnt0[t];
+                x = ex0[t];
+                if (p.spec) { p.cmode[t] = 1; p.pre_n[t] = 0; p.spec_from[t] = 0; }
+            } else {
+                resolve_entry<E, D>(p, sm, t, e, cnt0[t], ex0[t], cnt1[t], ex1[t], c, x);
+            }
+            if (t < p.n_warm) c = 0;  // a warm-up segment emits nothing
+            cnt[t] = c;
+            ex[t] = x;
+            if (x != prev_ex[t]) atomicOr(&res->flag, 1u);
+        }
     }
-    entry[t] = e;
-    u64 c;
-    u32 x;
-    if (e == 0) {
-        c = cnt0[t];
-        x = ex0[t];
-        if (p.spec) { p.cmode[t] = 1; p.pre_n[t] = 0; p.spec_from[t] = 0; }
-    } else {
-        resolve_entry<E, D>(p, sm, t, e, cnt0[t], ex0[t], cnt1[t], ex1[t], c, x);
+    c = warp_sum64(c);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u64 tot = 0;
+#pragma unroll
+        for (int w = 0; w < BLOCK / 32; w++) tot += wsum[w];
+        bsum[blockIdx.x] = tot;
+        if (tot) atomicAdd((unsigned long long *)&res->total, (unsigned long long)tot);
     }
-    cnt[t] = c;
-    ex[t] = x;
-    if (x != prev_ex[t]) atomicOr(&res->flag, 1u);
 }
 
 // emit: re-parse from the true entry and write this segment's samples at their
 // global offsets (exclusive scan of the counts).
 template <int E, int D>
 __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constant__ FillPlan p, const u32 *entry, const u64 *cnt,
-                                                const u64 *off, const u32 *ex, DevResult *res) {
+                                                const u64 *bsum, const u32 *ex, DevResult *res) {
     __shared__ ZigFast sm[256];
     __shared__ __align__(16) unsigned char ring_sm[2 * EMIT_GB * BLOCK];  // RingWriter: 32 B, BatchRing: 2 groups per thread
     stage_tables(p, sm);
     u32 t = blockIdx.x * BLOCK + threadIdx.x;
+    const u64 my_cnt = t < p.T ? cnt[t] : 0;
+    const u64 my_off = block_offset(bsum, my_cnt);
     Tally tl = {0, 0, 0, 0, 0};
     bool cp = false;
     if constexpr (D == FAM_GAMMA) {
@@ -1069,8 +1120,8 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constan
             const u32 lane = threadIdx.x & 31;
             u64 o = 0, c = 0, endp = 0;
             if (t < p.T) {
-                o = off[t];
-                c = cnt[t];
+                o = my_off;
+                c = my_cnt;
                 cp = o < p.n && c > 0 && p.cmode[t];
                 if (cp && o + c >= p.n) {  // holds sample n-1: the position after it
                     if (o + c == p.n) {
@@ -1158,7 +1209,7 @@ __global__ void __launch_bounds__(BLOCK, minb(E, D)) k_emit(const __grid_constan
         }
     }
     if (t < p.T) {
-        u64 o = off[t], c = cnt[t];
+        u64 o = my_off, c = my_cnt;
         if (t == p.T - 1) {
             res->total = o + c;
             res->next_start = seg_end(p, t) + ex[t];
