@@ -65,6 +65,10 @@ struct DevCtx {
     size_t spec_bytes = 0;
     void *pre = nullptr;
     size_t pre_bytes = 0;
+    // single-pass tile parse: one record per tile (+ the prefix record), tagged with a launch epoch
+    u64 *tile_rec = nullptr;
+    size_t tile_rec_n = 0;
+    u32 tile_epoch = 0;
     // the counted slice of rs_range_count, waiting for rs_range_emit (its plan refers to
     // the scratch above, so any other fill on this device invalidates it)
     struct Range {
@@ -718,6 +722,82 @@ rs_status prep_chunk(DevCtx &c, FillPlan &p, const Resolved &r, bool mem, cudaSt
     return RS_OK;
 }
 
+// One chunk through the single-pass tile parse: `words` engine words from the chunk's origin
+// (p.base), the buffered prefix ahead of them (p.P, first chunk) or p.lp0 words to skip.
+// On return c.res_host holds the result record; fell_back = the chunk left the tile model
+// (or the grid could not be made co-resident) and must be redone by the two-pass path.
+constexpr u64 TILE_MIN_N = 1ULL << 16;  // far above the 144-word prefix: sample n - 1 lies in a tile
+rs_status run_tile_chunk(DevCtx &c, FillPlan &p, const void *fn, u64 words, cudaStream_t st, bool &fell_back) {
+    static std::map<std::pair<int, const void *>, int> occ_cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto key = std::make_pair(dev, fn);
+    auto it = occ_cache.find(key);
+    int occ;
+    if (it == occ_cache.end()) {
+        occ = 0;
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TL_SMEM) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, TL_T, TL_SMEM) != cudaSuccess) {
+            cudaGetLastError();
+            occ = 0;
+        }
+        occ_cache[key] = occ;
+    } else {
+        occ = it->second;
+    }
+    fell_back = true;
+    if (occ < 1) return RS_OK;
+    const u64 TW = (u64)TL_T * TL_W;
+    const u64 NT = (words + TW - 1) / TW;
+    if (NT >= (1ULL << 31)) return RS_OK;
+    u64 G = (u64)c.sms * (u64)occ;
+    if (G > (u64)TL_T) G = TL_T;  // one record load per thread in the finish
+    if (G > NT) G = NT;
+    rs_status rc = plan_segments(c, p, 0, 0, 0, st, true, 36, TL_W, (G * TL_T + BLOCK - 1) / BLOCK * BLOCK);
+    if (rc) return rc;
+    if (p.engine == RS_ENG_PCG64) {
+        u128 inc = ((u128)p.base[3] << 64) | p.base[2], m, a;
+        rs::pcg_affine(inc, (u128)G * TW, m, a);
+        p.tile_m[0] = (u64)m; p.tile_m[1] = (u64)(m >> 64);
+        p.tile_a[0] = (u64)a; p.tile_a[1] = (u64)(a >> 64);
+    } else if (p.engine == RS_ENG_PHILOX) {
+        for (int i = 0; i < 10; i++) {  // round keys k + r*W (counter.py:95-96)
+            p.rk0[i] = p.base[4] + (u64)i * 0x9E3779B97F4A7C15ULL;
+            p.rk1[i] = p.base[5] + (u64)i * 0xBB67AE8584CAA73BULL;
+        }
+    }
+    if (NT + 1 > c.tile_rec_n) {
+        cudaFree(c.tile_rec);
+        c.tile_rec = nullptr;
+        c.tile_rec_n = 0;
+        const size_t cap = (size_t)(NT + 1) + (NT + 1) / 8 + 1024;
+        CK(cudaMalloc(&c.tile_rec, cap * 8));
+        CK(cudaMemsetAsync(c.tile_rec, 0, cap * 8, st));
+        c.tile_rec_n = cap;
+        c.tile_epoch = 0;
+    }
+    if (++c.tile_epoch == 0) {  // the epoch wrapped: clear the records once
+        CK(cudaMemsetAsync(c.tile_rec, 0, c.tile_rec_n * 8, st));
+        c.tile_epoch = 1;
+    }
+    p.tile_rec = c.tile_rec;
+    p.tile_nt = (u32)NT;
+    p.tile_epoch = c.tile_epoch;
+    CK(cudaMemsetAsync(c.res, 0, offsetof(DevResult, serial_state), st));
+    DevResult *res = c.res;
+    void *args[] = {&p, &res};
+    if ((rc = launch(fn, dim3((unsigned)G), dim3(TL_T), args, st, TL_SMEM))) return rc;
+    CK(cudaMemcpyAsync(c.res_host, c.res, offsetof(DevResult, serial_state), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    fell_back = c.res_host->pad != 0;
+    if (getenv("RS_TILE_DEBUG"))
+        fprintf(stderr, "[tile] NT=%llu G=%llu P=%d lp0=%llu n=%llu total=%llu end=%llu next=%llu pad=%u\n", (unsigned long long)NT,
+                (unsigned long long)G, p.P, (unsigned long long)p.lp0, (unsigned long long)p.n,
+                (unsigned long long)c.res_host->total, (unsigned long long)c.res_host->end_pos,
+                (unsigned long long)c.res_host->next_start, c.res_host->pad);
+    return RS_OK;
+}
+
 // The device part of one fill. On return (sync=true) `E` holds the stream units
 // consumed (64-bit words, or 32-bit halves incl. a used pending half when r.unit == 2)
 // and `tal` the tallies.
@@ -808,6 +888,10 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
     // pending half (u = 2) and the P buffered words, then the engine; a later chunk
     // has neither and lp counts engine units from its origin (thread 0 starts at lp0).
     VarKernels K = var_kernels(s->engine, r.family);
+    const void *tile_fn = nullptr;
+    if (sync && u == 1 && (r.family == FAM_NORM || r.family == FAM_EXP) && !(r.family == FAM_NORM && r.kind == NK_SKEW) &&
+        getenv("RS_TILE"))  // (opt-in until it beats the two-pass path)
+        tile_fn = rsk::tile_kernel(s->engine, r.family);
     const u64 P1 = (u64)p.P, pp1 = (u64)p.pending_used;
     u64 done = 0;    // samples produced so far
     u64 origin = 0;  // engine words from s->state to this chunk's origin (multiple of 36)
@@ -833,6 +917,27 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
         p.lp0 = lp0;
         p.n = need;
         p.out0 = done;
+        if (tile_fn && need >= TILE_MIN_N) {
+            // single-pass tile parse (rs_tile.cuh); a chunk outside its model (flag) is redone below
+            bool fell_back = false;
+            if ((rc = run_tile_chunk(c, p, tile_fn, words + lp0, st, fell_back))) return rc;
+            if (!fell_back) {
+                chunks++;
+                for (int i = 0; i < 6; i++) tal[i] += c.res_host->tally[i];
+                const u64 total = c.res_host->total;
+                const u64 to_engine = first ? (u64)0 - (u * P1 + pp1) : u * origin;
+                if (done + total >= n) {
+                    E = u * P1 + pp1 + (c.res_host->end_pos + to_engine);
+                    break;
+                }
+                done += total;
+                const u64 resume = c.res_host->next_start + to_engine;
+                origin = resume / u / 72 * 72;
+                lp0 = resume - u * origin;
+                first = false;
+                continue;
+            }
+        }
         int occ = std::min(occupancy(K.count), std::min(occupancy(K.fixup), occupancy(K.emit)));
         const bool mem = parse_from_memory(s->engine);
         rc = plan_segments(c, p, words + (lp0 + u - 1) / u, Lmin, occ, st, !mem);

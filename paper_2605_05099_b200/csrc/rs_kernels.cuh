@@ -90,7 +90,15 @@ struct FillPlan {
     u32 *mrank0;                  // phase-0 sample index at the merge point
     // counted ranges: the first n_warm segments only resolve the slice's entry (count 0)
     u32 n_warm;
+    // single-pass tile parse (rs_tile.cuh): tile records, tiles in the chunk, launch epoch,
+    // and PCG64's affine step from one of a CTA's tiles to its next (G tiles on)
+    u64 *tile_rec;
+    u32 tile_nt, tile_epoch;
+    u64 tile_m[2], tile_a[2];
 };
+// tile geometry of the single-pass parse: threads per CTA, words per thread and tile
+constexpr int TL_T = 512, TL_W = 16;
+constexpr size_t TL_SMEM = (size_t)(2 * TL_T + 2) * (TL_W + 1) * 8;
 // per-sample tally word of the gamma attempt machine: gamma attempts (8 bits), normal
 // attempts (12), normal pdf evaluations (12); 0xFFFFFFFF never occurs (flagged instead)
 __device__ __forceinline__ bool pack_tally(u32 ga, u32 na, u32 np, u32 &w) {
@@ -2000,6 +2008,7 @@ VarKernels var_kernels_x256ss(int fam);  // k_var_x256ss.cu
 VarKernels var_kernels_x256pp(int fam);  // k_var_x256pp.cu
 VarKernels var_kernels_pcg(int fam);     // k_var_pcg.cu
 VarKernels var_kernels_mem(int fam);     // k_var_mem.cu
+const void *tile_kernel(int engine, int fam);    // k_tile.cu: single-pass normal / exponential (pcg64, philox), else null
 const void *fixed_kernel(int engine, int mode);  // k_fixed.cu
 const void *philox_kernel(int mode);             // k_fixed.cu
 const void *simd_kernel(int engine, int mode);   // k_fixed.cu
