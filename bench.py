@@ -312,7 +312,8 @@ def run_ours(args, rank, world, local_rank):
 
     per_config = None
     if world == 1 and not args.no_per_config:
-        per_config = run_per_config(dev, stream, sptr, out64, peak, args.cpu_seconds, not args.no_cpu)
+        per_config = run_per_config(dev, stream, sptr, out64, peak, args.cpu_seconds, not args.no_cpu,
+                                    clocks.get("sm_max_mhz") or 1965.0)
     sharded = None
     if world > 1 and not args.no_per_config:
         sharded = run_sharded(rank, world, dev)
@@ -398,7 +399,7 @@ def run_sharded(rank, world, dev, reps=3):
             "timing": "wall clock per rank around fill_sharded (host-synchronising protocol), max over ranks"}
 
 
-def run_per_config(dev, stream, sptr, buf, peak, cpu_seconds, cpu=True):
+def run_per_config(dev, stream, sptr, buf, peak, cpu_seconds, cpu=True, issue_mhz=1965.0):
     """Every BASELINE row at its stated size, timed through the product call (Rng.fill with
     a device `out`, fill_streams, Rng.mvn): CUDA events on the stream around the
     synchronous call, best of 3 after a warm-up. Beside each: the fraction of the store-only
@@ -532,6 +533,29 @@ def run_per_config(dev, stream, sptr, buf, peak, cpu_seconds, cpu=True):
             "contraction_frac_of_dgemm_peak": tri / (ms_k / 1e3) / 1e12 / tf,
             "contraction_kernel": "k_mvn_dmma (mma.sync f64 / DMMA.8x8x4; triangular skip)",
             "cpu": cpu_r}
+    # Issue roofline of every row whose ceiling is instruction issue, not HBM (parse kernels,
+    # per-stream Lemire, the integer-bound engines): warp instructions of one fill (ncu
+    # smsp__inst_executed.sum over the fill's kernels, profiles/r02_issue_counts.json) / the
+    # row's time measured above, against one warp instruction per SMSP per cycle.
+    prof = os.path.join(ROOT, "profiles", "r02_issue_counts.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            counts = json.load(f)["configs"]
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        ipeak = sms * 4 * issue_mhz * 1e6 / 1e9  # G warp instructions / s
+        for label, c in counts.items():
+            if label in res and "ms" in res[label] and c.get("warp_instr"):
+                ach = c["warp_instr"] / (res[label]["ms"] / 1e3) / 1e9
+                res[label]["issue_roofline"] = {
+                    "bound": "issue", "warp_instr_per_sample": c["warp_instr"] / res[label]["n"],
+                    "lanes_per_warp_instr": c["thread_instr"] / c["warp_instr"],
+                    "achieved": ach, "peak": ipeak, "unit": "G warp instructions/s", "frac": ach / ipeak,
+                    "peak_source": "%d SMs x 4 SMSPs x 1 warp instruction/cycle x %.0f MHz" % (sms, issue_mhz),
+                    "source": "profiles/r02_issue_counts.json (ncu --metrics smsp__inst_executed.sum, same fill)"}
+        z = counts.get("c5a_z_philox_norm_2p29")
+        if z:
+            res["c5a_z_fill_instr"] = {"warp_instr": z["warp_instr"], "n": 1 << 29,
+                                       "note": "the z fill of C5a d = 512 (2^29 Philox normals): materialise + count + emit"}
     return res
 
 

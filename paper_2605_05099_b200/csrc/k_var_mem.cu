@@ -10,8 +10,9 @@ rsk::VarKernels vk() {
 
 rsk::VarKernels rsk::var_kernels_mem(int fam) {
     switch (fam) {
-    case FAM_NORM: return vk<FAM_NORM>();
-    case FAM_EXP: return vk<FAM_EXP>();
+    // the word-level 8-word batch parses read a whole batch ahead (EngMemB)
+    case FAM_NORM: return rsk::VarKernels{(const void *)k_count<RS_ENG_MEMB, FAM_NORM>, (const void *)k_fixup<RS_ENG_MEMB, FAM_NORM>, (const void *)k_emit<RS_ENG_MEMB, FAM_NORM>};
+    case FAM_EXP: return rsk::VarKernels{(const void *)k_count<RS_ENG_MEMB, FAM_EXP>, (const void *)k_fixup<RS_ENG_MEMB, FAM_EXP>, (const void *)k_emit<RS_ENG_MEMB, FAM_EXP>};
     case FAM_GAMMA: return vk<FAM_GAMMA>();
     case FAM_F32: return vk<FAM_F32>();
     case FAM_U32: return vk<FAM_U32>();
