@@ -535,7 +535,6 @@ class Rng:
         dev = self._device()
 
         def factorise():
-            symmetric()
             f = np.ascontiguousarray(semidefinite_factor(cov))
             return f, not np.triu(f, 1).any()
 
@@ -544,11 +543,22 @@ class Rng:
         # The reference factorises before drawing (continuous.py:331), so a failed
         # factorisation puts the generator back where it was: nothing observable is consumed.
         before = (list(self.engine.s), self.buffer.capture(), {k: dict(v) for k, v in self.counters.items()})
+        # (two host workers: the symmetry check and the factorisation each take about as long
+        # as half the z fill at d = 512; its error is the earlier one in the reference's order)
+        fsym = _host_pool().submit(symmetric)
         fut = _host_pool().submit(factorise)
         try:
             self.device_fill("stdnorm", [], [], n * d, out=z)
         finally:
             try:
+                sym_err = fsym.exception()
+                if sym_err is not None:
+                    fut.cancel()
+                    try:
+                        fut.result()  # (let a running factorisation finish before the state is restored)
+                    except Exception:
+                        pass
+                    raise sym_err
                 factor, lower = fut.result()
             except Exception:
                 self.engine.s, self.counters = before[0], before[2]
@@ -567,12 +577,12 @@ _POOL = None
 
 
 def _host_pool():
-    """One worker thread for host work that overlaps a device fill (mvn's factorisation)."""
+    """Two worker threads for host work that overlaps a device fill (mvn's symmetry check and factorisation)."""
     global _POOL
     if _POOL is None:
         import concurrent.futures
 
-        _POOL = concurrent.futures.ThreadPoolExecutor(1, thread_name_prefix="randstream-host")
+        _POOL = concurrent.futures.ThreadPoolExecutor(2, thread_name_prefix="randstream-host")
     return _POOL
 
 
