@@ -494,6 +494,9 @@ def run_per_config(dev, stream, sptr, buf, peak, cpu_seconds, cpu=True, issue_mh
     # C5a: mvn, d in {64, 256, 512}, n = 2^20 (the BASELINE recipe: philox seed 31, S from the
     # same r, mvn on the same r). Whole call (z draw overlapping the host Cholesky, then the
     # contraction) and the contraction alone (rs_mvn_apply: k_mvn_dmma, FP64 tensor cores)
+    # (all three GPU timings first: the CPU leg's OpenBLAS threads keep spinning for a while
+    # after a call and slowed the next row's host-side symmetry check and Cholesky by 2-4 ms)
+    mvn_rows = {}
     for d in (64, 256, 512):
         n = 1 << 20
         r = state_io.create("philox", seed=[31])
@@ -507,7 +510,13 @@ def run_per_config(dev, stream, sptr, buf, peak, cpu_seconds, cpu=True, issue_mh
         ms_k = timed(lambda: _lib.check(_lib.lib.rs_mvn_apply(
             ctypes.c_void_p(Lf.ctypes.data), mean.ctypes.data_as(_lib.DBLP), d, n, 0, ctypes.c_void_p(z.data_ptr()),
             ctypes.c_void_p(X.data_ptr()), sptr)))
-        del z, X
+        zt = torch.empty(n * d, dtype=torch.float64, device=dev)
+        ms_z = timed(lambda: r.device_fill("stdnorm", [], [], n * d, out=zt))
+        del z, X, zt
+        mvn_rows[d] = (ms_all, ms_k, ms_z, Lf)
+    for d in (64, 256, 512):
+        n = 1 << 20
+        ms_all, ms_k, ms_z, Lf = mvn_rows[d]
         tri = n * d * (d + 1)
         cpu_r = None
         if cpu:  # the reference's CPU path: z by the port (P threads), X = z @ L^T by numpy
@@ -527,7 +536,8 @@ def run_per_config(dev, stream, sptr, buf, peak, cpu_seconds, cpu=True, issue_mh
                      "how": "z by the port on P threads + numpy z @ L^T (OpenBLAS), 2^14 vectors per call"}
         res["c5a_mvn_d%d_2p20" % d] = {
             "vectors_per_s": n / (ms_all / 1e3), "ms": ms_all,
-            "timed": "Rng.mvn(0, S, 2^20): z fill + host Cholesky (overlapped) + contraction",
+            "timed": "Rng.mvn(0, S, 2^20): z fill + host symmetry check and Cholesky (overlapped) + contraction",
+            "z_fill_ms": ms_z, "z_fill_gsamples_s": n * d / (ms_z / 1e3) / 1e9,
             "contraction_ms": ms_k, "contraction_tflops_triangular": tri / (ms_k / 1e3) / 1e12,
             "contraction_tflops_dense_equiv": 2.0 * n * d * d / (ms_k / 1e3) / 1e12,
             "contraction_frac_of_dgemm_peak": tri / (ms_k / 1e3) / 1e12 / tf,
@@ -553,9 +563,15 @@ def run_per_config(dev, stream, sptr, buf, peak, cpu_seconds, cpu=True, issue_mh
                     "peak_source": "%d SMs x 4 SMSPs x 1 warp instruction/cycle x %.0f MHz" % (sms, issue_mhz),
                     "source": "profiles/r02_issue_counts.json (ncu --metrics smsp__inst_executed.sum, same fill)"}
         z = counts.get("c5a_z_philox_norm_2p29")
-        if z:
-            res["c5a_z_fill_instr"] = {"warp_instr": z["warp_instr"], "n": 1 << 29,
-                                       "note": "the z fill of C5a d = 512 (2^29 Philox normals): materialise + count + emit"}
+        row512 = res.get("c5a_mvn_d512_2p20")
+        if z and row512 and row512.get("z_fill_ms"):
+            ach = z["warp_instr"] / (row512["z_fill_ms"] / 1e3) / 1e9
+            row512["z_fill_issue_roofline"] = {
+                "bound": "issue", "warp_instr_per_sample": z["warp_instr"] / float(1 << 29),
+                "lanes_per_warp_instr": z["thread_instr"] / z["warp_instr"],
+                "achieved": ach, "peak": ipeak, "unit": "G warp instructions/s", "frac": ach / ipeak,
+                "note": "2^29 Philox normals: materialise (integer-bound) + count + emit over the words",
+                "source": "profiles/r02_issue_counts.json"}
     return res
 
 

@@ -869,3 +869,29 @@ def test_integration_device_fill(engine, dist, params):
     Lf = np.linalg.cholesky(S)
     assert np.max(np.abs(X - z @ Lf.T) / (np.abs(z) @ np.abs(Lf).T)) <= 1e-12
     _assert_same_position(ref_like, o)
+
+
+@pytest.mark.parametrize("engine,dist,params,n", [
+    ("pcg64", "norm", {}, 1 << 16), ("pcg64", "norm", {"mu": 1.5, "var": 2.0}, (1 << 21) + 77),
+    ("philox", "norm", {}, 1 << 20), ("pcg64", "exp", {}, (1 << 21) + 5), ("philox", "exp", {"beta": 0.5}, (1 << 21) + 6)])
+def test_tile_parse_opt_in(engine, dist, params, n, monkeypatch):
+    """The single-pass tile parse (csrc/rs_tile.cuh, RS_TILE=1; measured slower than the two-pass
+    path and therefore opt-in, DESIGN 4.7) gives the reference's samples, position and
+    tallies: from a fresh stream and mid-buffer, with a chained second fill that starts on a
+    buffered prefix, and through its flagged fallback (a normal tail across a tile edge)."""
+    monkeypatch.setenv("RS_TILE", "1")
+    for pre in (0, 5):
+        r = state_io.create(engine, seed=[99])
+        o = O.OracleRng(engine, seed=[99])
+        for _ in range(pre):
+            assert r.next_u64() == o.next_u64()
+        got = _np(r.fill(dist, params, n))
+        ref = o.fill(dist, params, n)
+        diff = np.nonzero(_bits(got) != _bits(ref))[0]
+        assert len(diff) == 0, "first diff at %d" % diff[0]
+        _assert_same_position(r, o)
+        assert r.counters == o.tallies()
+        got2 = _np(r.fill(dist, params, 70000))
+        assert np.array_equal(_bits(got2), _bits(o.fill(dist, params, 70000)))
+        _assert_same_position(r, o)
+        assert r.counters == o.tallies()
