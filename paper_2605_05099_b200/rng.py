@@ -14,6 +14,7 @@ fills. After any fill the engine state and buffer equal the reference's
 
 import ctypes
 import math
+import warnings
 from functools import wraps
 from struct import pack, unpack
 
@@ -71,6 +72,22 @@ _SIGNATURES = {
     "skew_normal": (("alpha", "mu", "sigma"), ()),
 }
 _TALLY_NAMES = ("norm", "exp", "gamma")
+
+# Engines without skip-ahead (sfc.py / rng.py:162-163: "jump unsupported"): one stream cannot
+# be split over GPU threads, so a single-stream fill replays it on ONE device thread
+# (~10 Msamples/s). Their parallel form is per-stream mode (fill_streams: one spawned stream
+# per thread, C5b). Warn once per engine when such a fill is large enough to matter.
+_SERIAL_ENGINES = ("sfc64", "sfc64simd", "cwg128")
+_SERIAL_WARN_N = 1 << 16
+_serial_warned = set()
+
+
+def _warn_serial(eid):
+    if eid not in _serial_warned:
+        _serial_warned.add(eid)
+        warnings.warn("%s has no skip-ahead: a single-stream device fill runs on one GPU thread (~10 Msamples/s); "
+                      "use fill_streams (one spawned stream per thread) for bulk draws" % eid, RuntimeWarning,
+                      stacklevel=4)
 
 
 def _op(fn):
@@ -353,6 +370,8 @@ class Rng:
         n = int(n)
         if n < 0:
             raise ValueError("draw count must be >= 0")
+        if n >= _SERIAL_WARN_N and self.engine_id in _SERIAL_ENGINES:
+            _warn_serial(self.engine_id)
         if dist in SCALAR_NAMES:
             fp = self._continuous_params(dist, params, n)
             return self.device_fill(dist, fp, [], n, out)

@@ -300,3 +300,17 @@ def test_tables_header_matches_reference_zigtables():
         sys.argv = argv
     text = (ROOT / "paper_2605_05099_b200" / "csrc" / "rs_tables.h").read_text()
     assert g["render"]() == text
+
+
+def test_serial_engine_warning_text():
+    """Engines without skip-ahead warn once when a large single-stream fill is requested
+    (the fill itself needs a GPU; here only the bookkeeping)."""
+    import warnings as W
+    from paper_2605_05099_b200 import rng as R
+    R._serial_warned.discard("sfc64")
+    with W.catch_warnings(record=True) as got:
+        W.simplefilter("always")
+        R._warn_serial("sfc64")
+        R._warn_serial("sfc64")
+    assert len(got) == 1 and "fill_streams" in str(got[0].message)
+    assert set(R._SERIAL_ENGINES) == {"sfc64", "sfc64simd", "cwg128"}
