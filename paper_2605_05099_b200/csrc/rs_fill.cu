@@ -581,17 +581,29 @@ rs_status launch_simd(DevCtx &c, FillPlan &p, int mode, cudaStream_t st) {
     const void *fn = simd_kernel(p.engine, mode);
     u64 steps = (p.weng + 7) / 8;
     if (steps == 0) steps = 1;
-    // an eighth of a wave of lane-threads: the per-lane GF(2) setup (k_x256_setup) costs
-    // per thread, while the store-bound fill saturates HBM well before a full wave
-    // (x256++simd 2^28 normals 3.86 -> 3.71 ms, 2^24 raw 0.28 -> 0.09 ms)
-    u64 Gfull = (u64)c.sms * occupancy(fn) * BLOCK / 64;
-    u64 Ls = (steps + Gfull - 1) / Gfull;
+    // Lane-thread groups: >= 128 steps per thread amortise the per-thread GF(2) setup
+    // (k_x256_setup), capped at ONE block per SM: 148 x 32 groups, each a stream of 256-byte
+    // runs, measured faster than 2, 3, 4 or 6 blocks per SM at every size from 2^26 up
+    // (raw 2^30: 1.37 / 1.39 / 1.82 / 1.47 / 1.48 ms), and than the earlier 96 blocks, which
+    // left a third of the SMs idle (1.83 ms).
+    u64 blocks = ((steps + 127) / 128 + 31) / 32;
+    if (blocks > (u64)c.sms) blocks = c.sms;
+    u64 G = blocks * (BLOCK / 8);
+    u64 Ls = (steps + G - 1) / G;
     if (Ls < 16) Ls = 16;
-    u64 G = (steps + Ls - 1) / Ls;
+    Ls = (Ls + 3) / 4 * 4;  // whole 4-step batches (256-byte runs)
+    G = (steps + Ls - 1) / Ls;
     u64 Gpad = (G + BLOCK - 1) / BLOCK * BLOCK;
     p.L = Ls;
     p.G = G;
     p.Gpad = Gpad;
+    {   // 256-byte runs need the group's first word 32-byte aligned and every sample to exist
+        // as a whole element (half modes: an even count after the pending half)
+        const bool half = mode == FX_U01F || mode == FX_HMAP;
+        uintptr_t a0 = (uintptr_t)p.out + (half ? 4 * ((u64)p.pending_used + 2ULL * p.P) : 8ULL * p.P);
+        const u64 need = half ? (u64)p.pending_used + 2ULL * ((u64)p.P + p.weng / 8 * 8) : (u64)p.P + p.weng / 8 * 8;
+        p.vec_ok = (a0 & 31) == 0 && need <= p.n;
+    }
     rs_status rc = ensure_scratch(c, 8 * Gpad);
     if (rc) return rc;
     int lv = 0;
@@ -879,7 +891,14 @@ rs_status run_fill(DevCtx &c, const rs_stream *s, const Resolved &r, u64 n, void
             return RS_OK;
         }
         const void *fn = fixed_kernel(s->engine, r.fixed_mode);
-        rc = plan_segments(c, p, p.weng ? p.weng : 1, 64, occupancy(fn, FX_SMEM), st, true, 144);
+        int focc = occupancy(fn, FX_SMEM);
+        if (s->engine == RS_ENG_X256SS || s->engine == RS_ENG_X256PP || s->engine == RS_ENG_X128P || s->engine == RS_ENG_XORO) {
+            // the GF(2) jump setup costs per thread: below ~1500 words per thread fewer resident
+            // blocks win (x256** raw 2^26: 0.240 ms at 3 blocks/SM, 0.183 at 1; 2^30 keeps 3)
+            const u64 k = p.weng / ((u64)c.sms * BLOCK * 1536);
+            focc = (int)std::max<u64>(1, std::min<u64>((u64)focc, k));
+        }
+        rc = plan_segments(c, p, p.weng ? p.weng : 1, 64, focc, st, true, 144);
         if (rc) return rc;
         if ((rc = launch_fixed(c, p, fn, st))) return rc;
         E = n;

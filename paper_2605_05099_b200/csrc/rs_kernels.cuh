@@ -1612,6 +1612,30 @@ __global__ void __launch_bounds__(BLOCK) k_simd_fixed(const __grid_constant__ Fi
     e.load(p.x256_states + 4 * (k * p.Gpad + g));
     const u64 steps = (p.weng + 7) / 8;
     u64 s0 = g * p.L, s1 = s0 + p.L < steps ? s0 + p.L : steps;
+    // A group's 8 threads emit 64 contiguous bytes per step and consecutive steps are adjacent,
+    // so 4 steps staged in shared memory leave as one 256-byte run per group: each thread
+    // stores 32 bytes of it (a store-only probe: 64-byte runs 4.5 TB/s, 256-byte runs 5.8,
+    // DESIGN 4.3). Needs 32-byte aligned runs (p.vec_ok) and whole steps; the rest goes word by word.
+    if (p.vec_ok) {
+        __shared__ __align__(16) u64 stg[BLOCK / 8][34];
+        u64 *row = stg[threadIdx.x >> 3];
+        u64 *out = (u64 *)p.out;
+        const unsigned gmask = 0xFFu << (threadIdx.x & 24);  // my group's 8 lanes (groups differ in trip count)
+        const u64 whole = p.weng / 8;  // steps whose 8 words all exist
+        const u64 sv = s1 < whole ? s1 : whole;
+        for (; s0 + 4 <= sv; s0 += 4) {
+#pragma unroll
+            for (int i = 0; i < 4; i++) row[8 * i + k] = fx_map<MODE>(p, e.next());
+            __syncwarp(gmask);
+            const ulonglong2 a = *(const ulonglong2 *)&row[4 * k], b = *(const ulonglong2 *)&row[4 * k + 2];
+            u64 *dst;
+            if constexpr (is_half(MODE)) dst = (u64 *)((u32 *)out + p.pending_used) + (u64)p.P + 8 * s0 + 4 * k;
+            else dst = out + (u64)p.P + 8 * s0 + 4 * k;
+            asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "l"(a.x), "l"(a.y), "l"(b.x), "l"(b.y)
+                         : "memory");
+            __syncwarp(gmask);
+        }
+    }
     for (u64 st = s0; st < s1; st++) {
         u64 q = fx_map<MODE>(p, e.next());
         u64 j = 8 * st + k;
