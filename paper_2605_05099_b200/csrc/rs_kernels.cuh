@@ -1876,6 +1876,59 @@ __device__ __forceinline__ void stream_rows8(u64 *out, u64 j, u64 nper, bool val
 // sit the store out). A lane adds <= 32 samples between stores, so the ring never holds
 // more than 63. The per-sample redraw loop instead kept every lane waiting for the
 // warp's slowest sample (m = 2^63 + 1 rejects half of the words).
+// Lemire rows whose bound rejects (almost) never (threshold <= 2^44: a rejection rate of at
+// most 2^-20; larger thresholds keep the redraw loops or the ring form below): a chunk takes one word per sample with no redraw
+// loop -- straight-line code the compiler schedules across samples -- and a chunk that did
+// see a rejected word (b = 6: 2^-62 per word) is redone from the saved engine with the
+// exact loop.
+template <class D, class EN>
+__device__ __forceinline__ void stream_rows_lemire_spec(u64 *out, u64 j, u64 nper, bool valid, u64 *tile, const D &d,
+                                                        EN &e) {
+    const u32 lane = threadIdx.x & 31;
+    const u64 nch = nper / FX_CH;
+    const u64 row = (u64)(uintptr_t)(out + j * nper);
+    for (u64 k = 0; k < nch; k++) {
+        if (valid) {
+            const EN e0 = e;
+            u64 *q = tile + fx_at(lane, 0), *const qe = q + FX_CH;
+            bool ok = true;
+#pragma unroll 8
+            while (q < qe) {
+                u64 o;
+                ok &= d.accept(e.next(), o);
+                *q++ = o;
+            }
+            if (!ok) {
+                e = e0;
+                q = tile + fx_at(lane, 0);
+                while (q < qe) {
+                    u64 o;
+                    while (!d.accept(e.next(), o)) {}
+                    *q++ = o;
+                }
+            }
+        }
+        __syncwarp();
+        const u64 dst = valid ? row + k * FX_CH * 8 : 0;
+#pragma unroll
+        for (int g = 0; g < 16; g++) {
+            u32 r = 2 * g + (lane >> 4), c = lane & 15;
+            u64 dd = __shfl_sync(0xFFFFFFFFu, dst, r);
+            if (dd) {
+                u64 x = tile[fx_at(r, 2 * c)], y = tile[fx_at(r, 2 * c + 1)];
+                asm volatile("st.global.v2.b64 [%0], {%1, %2};" ::"l"(dd + 16 * c), "l"(x), "l"(y) : "memory");
+            }
+        }
+        __syncwarp();
+    }
+    if (valid)
+        for (u64 i = nch * FX_CH; i < nper; i++) {
+            u64 o;
+            while (!d.accept(e.next(), o)) {}
+            out[j * nper + i] = o;
+        }
+}
+
 template <class D, class EN>
 __device__ __forceinline__ void stream_rows_lemire(u64 *out, u64 j, u64 nper, bool valid, u64 *tile, const D &d,
                                                    EN &e) {
@@ -2032,13 +2085,17 @@ __global__ void __launch_bounds__(STR_BLOCK) k_streams(const __grid_constant__ S
         if (tiled) {
             if constexpr (D == FAM_LEMIRE_RING) {
                 stream_rows_lemire((u64 *)a.out, j, a.nper, valid, tile, d, e);
-            } else if constexpr (D == FAM_LEMIRE) {  // (almost) no rejections: unrolled 32-sample chunks
-                auto prod = [&]() {
-                    u64 o;
-                    while (!d.accept(e.next(), o)) {}
-                    return o;
-                };
-                stream_rows8((u64 *)a.out, j, a.nper, valid, tile, prod);
+            } else if constexpr (D == FAM_LEMIRE) {
+                if (d.thr <= (1ULL << 44)) {  // rejection rate <= 2^-20: speculative 32-sample chunks
+                    stream_rows_lemire_spec((u64 *)a.out, j, a.nper, valid, tile, d, e);
+                } else {  // up to 1/16 (above that the host picks the ring form): redraw loops
+                    auto prod = [&]() {
+                        u64 o;
+                        while (!d.accept(e.next(), o)) {}
+                        return o;
+                    };
+                    stream_rows8((u64 *)a.out, j, a.nper, valid, tile, prod);
+                }
             } else {  // 8-byte samplers are word-fed
                 auto prod = [&]() {
                     T v = d.sample(e, tl);

@@ -895,3 +895,20 @@ def test_tile_parse_opt_in(engine, dist, params, n, monkeypatch):
         assert np.array_equal(_bits(got2), _bits(o.fill(dist, params, 70000)))
         _assert_same_position(r, o)
         assert r.counters == o.tallies()
+
+
+def test_streams_lemire_speculative_chunk_redo():
+    """Per-stream Lemire rows take one word per sample without a redraw loop when the bound's
+    rejection rate is <= 2^-20, and redo a 32-sample chunk from the saved engine when it did
+    reject a word. b = 2^44 + 1 has the largest such rate (threshold 2^44 - 2^20 + 1): over
+    1024 streams x 8192 words about 8 words are rejected -- asserted -- so the redo runs."""
+    b, S, n = (1 << 44) + 1, 1024, 8192
+    thr = (1 << 64) % b
+    assert (1 << 43) < thr <= (1 << 44)
+    host = _np(fill_streams("sfc64", [31], [7], 0, S, "uint64", {"b": b}, n))
+    refs = O.threaded_fill([O.OracleRng("sfc64", seed=[31], spawn_key=(7, j)) for j in range(S)], "uint64", {"b": b}, n)
+    raw = O.threaded_fill([O.OracleRng("sfc64", seed=[31], spawn_key=(7, j)) for j in range(S)], "uint64", {}, n)
+    rejected = sum(int(np.count_nonzero(w * np.uint64(b) < np.uint64(thr))) for w in raw)
+    assert rejected >= 1, "the case must reject at least one word to exercise the redo"
+    for j in range(S):
+        assert np.array_equal(host[j], refs[j]), j
