@@ -607,8 +607,16 @@ def main():
     import torch.distributed as dist
 
     if world > 1:
+        # RS_BENCH_BACKEND=gloo: plumbing test of the N > 1 path on a box with fewer GPUs than
+        # ranks (ranks share devices; no kernel waits on another rank). Never a bench number.
+        backend = os.environ.get("RS_BENCH_BACKEND", "nccl")
+        if backend != "nccl":
+            local_rank = local_rank % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     line = run_ours(args, rank, world, local_rank)
     if rank == 0:
         if world == 1 and not args.no_cpu:

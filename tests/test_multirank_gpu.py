@@ -71,3 +71,28 @@ def test_two_process_device_ranges(engine, dist_name, params, n):
         assert st == o.get_state() and cap["words"] == words and cap["cursor"] == cursor
         assert cap["pending"] == pending
         assert counters == o.tallies()
+
+
+@pytest.mark.slow
+def test_bench_two_ranks_plumbing():
+    """bench.py's N > 1 path (the driver's torchrun launch line: barriers, max-over-ranks
+    time, one JSON line from rank 0, the sharded C3 line) with two ranks sharing this GPU
+    over gloo (RS_BENCH_BACKEND=gloo). A plumbing check only: the numbers mean nothing."""
+    import json
+    import pathlib
+    import subprocess
+    import sys
+
+    root = pathlib.Path(__file__).resolve().parents[1]
+    env = dict(os.environ, RS_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), str(root / "bench.py"), "--gpus", "2", "--steps", "2",
+           "--warmup", "3", "--no-e2e"]
+    p = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, "rank 0 prints exactly one JSON line"
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["steps"] == 2 and line["scaling"] == "weak"
+    assert line["value"] > 0 and line["sharded_c3"]["gsamples_s"] > 0
+    assert line["gpu_launches"] == 4
