@@ -107,11 +107,12 @@ struct EngPcg {  // pcg.py:25-39 (DXSM of the pre-step state; 64-bit "cheap" mul
         hi *= RS_PCG_MULT;
         hi ^= hi >> 48;
         u64 r = hi * lo;
-        u64 nlo = slo * RS_PCG_MULT;
-        u64 nhi = __umul64hi(slo, RS_PCG_MULT) + shi * RS_PCG_MULT;
-        u64 a = nlo + ilo;
-        nhi += ihi + (a < nlo ? 1ULL : 0ULL);
-        slo = a; shi = nhi;
+        // state * M + inc as one 128-bit expression: the carry into the high word rides the
+        // add chain (IADD3.X) instead of a compare + select (pcg64 raw 2^30 1.71 -> 1.61 ms,
+        // normals 2^28 2.01 -> 1.95 ms)
+        typedef unsigned __int128 U;
+        const U st = (((U)shi << 64) | slo) * (U)RS_PCG_MULT + (((U)ihi << 64) | ilo);
+        slo = (u64)st; shi = (u64)(st >> 64);
         return r;
     }
     // state <- mul*state + add (mod 2^128)
