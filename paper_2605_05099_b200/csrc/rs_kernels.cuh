@@ -596,7 +596,7 @@ __device__ __forceinline__ u64 wl_count(const D &d, SRC &s, u64 end, Tally &tl, 
 #pragma unroll
             for (int k = 0; k < 4; k++) {
                 F |= (d.zfast(w[h + k], f[k]) ? 1u : 0u) << (h + k);
-                Z |= ((w[h + k] & 0xFF) == 0 ? 1u : 0u) << (h + k);
+                Z |= (((u32)w[h + k] & 0xFFu) == 0 ? 1u : 0u) << (h + k);
             }
         }
         if (F == 0xFFu && m.st == 0) {
@@ -679,7 +679,7 @@ __device__ __forceinline__ void wl_emit(const D &d, SRC &s, u64 kmax, W &wr, Tal
 #pragma unroll
             for (int q = 0; q < 4; q++) {
                 F |= (d.zfast(w[h + q], f[q]) ? 1u : 0u) << (h + q);
-                Z |= ((w[h + q] & 0xFF) == 0 ? 1u : 0u) << (h + q);
+                Z |= (((u32)w[h + q] & 0xFFu) == 0 ? 1u : 0u) << (h + q);
                 x[h + q] = d.zval(w[h + q], f[q]);
             }
         }

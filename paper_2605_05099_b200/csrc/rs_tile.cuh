@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(TL_T, 1) k_tile(const __grid_constant__ FillPl
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
                         F |= (d.zfast(w[g + q], f[q]) ? 1u : 0u) << (g + q);
-                        Z |= ((w[g + q] & 0xFF) == 0 ? 1u : 0u) << (g + q);
+                        Z |= (((u32)w[g + q] & 0xFFu) == 0 ? 1u : 0u) << (g + q);
                         x[g + q] = d.zval(w[g + q], f[q]);
                     }
                 }
