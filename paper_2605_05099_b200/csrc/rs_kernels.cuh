@@ -602,6 +602,21 @@ __device__ __forceinline__ u64 wl_count(const D &d, SRC &s, u64 end, Tally &tl, 
         if (F == 0xFFu && m.st == 0) {
             cc += ZB;
             bnd = true;
+        } else if constexpr (std::is_same<decltype(s.e), EngMemB>::value) {
+            // materialised words are read again where they lie (L1 hits) instead of staged
+            const u64 *wp = s.e.w + (s.e.idx - ZB);
+            auto wg = [wp](int q) -> u64 { return __ldg(wp + q); };
+            u32 O, att;
+            double xc;
+            if (zb_tokens(d, m, wg, F, Z, O, att, bnd, xc, tl)) {
+                cc += __popc(O);
+            } else {
+                for (int k = 0; k < ZB; k++) {
+                    double z;
+                    bnd = d.feed(m, wg(k), tl, z);
+                    cc += bnd;
+                }
+            }
         } else {
 #pragma unroll
             for (int k = 0; k < ZB; k++) wsm[k * BLOCK] = w[k];
@@ -686,9 +701,17 @@ __device__ __forceinline__ void wl_emit(const D &d, SRC &s, u64 kmax, W &wr, Tal
         u32 O = 0xFFu;
         if (F != 0xFFu || m.st != 0) {
             const u32 fb = wr.free_base();
+            const u64 *wp = nullptr;
+            if constexpr (std::is_same<decltype(s.e), EngMemB>::value) {
+                wp = s.e.w + (s.e.idx - ZB);  // materialised words: read again where they lie
+            } else {
 #pragma unroll
-            for (int q = 0; q < ZB; q++) *wr.slot_at(fb + q) = w[q];
-            auto ws = [&wr, fb](int q) -> u64 { return *wr.slot_at(fb + (u32)q); };
+                for (int q = 0; q < ZB; q++) *wr.slot_at(fb + q) = w[q];
+            }
+            auto ws = [&wr, fb, wp](int q) -> u64 {
+                if constexpr (std::is_same<decltype(s.e), EngMemB>::value) return __ldg(wp + q);
+                else return *wr.slot_at(fb + (u32)q);
+            };
             u32 att;
             bool bnd;
             double xc = 0.0;
