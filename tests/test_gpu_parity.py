@@ -912,3 +912,22 @@ def test_streams_lemire_speculative_chunk_redo():
     assert rejected >= 1, "the case must reject at least one word to exercise the redo"
     for j in range(S):
         assert np.array_equal(host[j], refs[j]), j
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("engine,dist,n", [("x256**", "uint64", (1 << 32) + 12345), ("philox", "u01", (1 << 32) + 7),
+                                           ("pcg64", "norm", (1 << 31) + 1001)])
+def test_fills_beyond_2p32_samples(engine, dist, n):
+    """Maximum sizes: a fill of more than 2^32 samples (2^31 for the two-pass parse) equals two
+    chained fills split mid-buffer -- the chunk, grid and offset arithmetic at sizes no other
+    test reaches -- compared on the device, with the final position and tallies."""
+    free, _ = torch.cuda.mem_get_info()
+    if free < 2.2 * 8 * n:
+        pytest.skip("needs %.0f GiB of free device memory" % (2.2 * 8 * n / 2 ** 30))
+    n1 = n // 3 + 11
+    a, b = state_io.create(engine, seed=[5]), state_io.create(engine, seed=[5])
+    whole = a.fill(dist, {}, n)
+    p1 = b.fill(dist, {}, n1)
+    p2 = b.fill(dist, {}, n - n1)
+    assert torch.equal(whole[:n1], p1) and torch.equal(whole[n1:], p2)
+    assert a.get_state() == b.get_state() and a.buffer.capture() == b.buffer.capture() and a.counters == b.counters
