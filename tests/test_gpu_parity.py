@@ -931,3 +931,21 @@ def test_fills_beyond_2p32_samples(engine, dist, n):
     p2 = b.fill(dist, {}, n - n1)
     assert torch.equal(whole[:n1], p1) and torch.equal(whole[n1:], p2)
     assert a.get_state() == b.get_state() and a.buffer.capture() == b.buffer.capture() and a.counters == b.counters
+
+
+def test_fill_on_a_side_stream():
+    """Fills run on torch's current stream: on a side stream, consumed by later work queued on
+    that stream (no extra synchronisation), the samples and the position are the oracle's."""
+    side = torch.cuda.Stream()
+    for engine, dist, params, n in (("philox", "u01", {}, (1 << 20) + 3), ("x256**", "norm", {}, 1 << 19),
+                                    ("pcg64", "gamma", {"alpha": 2.5}, 1 << 17)):
+        r = state_io.create(engine, seed=[41])
+        o = O.OracleRng(engine, seed=[41])
+        with torch.cuda.stream(side):
+            out = r.fill(dist, params, n)
+            twice = out * 2.0  # queued behind the fill on the same stream
+        side.synchronize()
+        ref = o.fill(dist, params, n)
+        assert np.array_equal(_bits(_np(out)), _bits(ref)), (engine, dist)
+        assert np.array_equal(_np(twice), ref * 2.0)
+        _assert_same_position(r, o)
