@@ -949,3 +949,66 @@ def test_fill_on_a_side_stream():
         assert np.array_equal(_bits(_np(out)), _bits(ref)), (engine, dist)
         assert np.array_equal(_np(twice), ref * 2.0)
         _assert_same_position(r, o)
+
+
+def test_reference_behaviours_on_the_device_path():
+    """The properties the reference's own fill tests assert (pkg/tests/test_continuous.py:178-232,
+    :331-366, :412-445), on device fills: the uniform grids in both mantissa modes, the mantissa
+    mode changing the mapping but not the consumption, two u01f per word, a failed draw leaving
+    the position alone, the fill surface's errors, replays, and the MVN layout / rank-one /
+    rejection cases."""
+    # uniform grids (52 / 53 bits; 23 / 24 bits for f32), in [0, 1)
+    r = state_io.create("x256++", seed=[5])
+    u = _np(r.fill("u01", {}, 4096))
+    assert ((u >= 0) & (u < 1)).all() and np.array_equal(u * 2.0 ** 52, np.floor(u * 2.0 ** 52))
+    r.set_full_mantissa(True)
+    s = _np(r.fill("u01", {}, 4096)) * 2.0 ** 53
+    assert np.array_equal(s, np.floor(s)) and (s.astype(np.int64) & 1).any()
+    uf = _np(r.fill("u01f", {}, 4096)).astype(np.float64) * 2.0 ** 24
+    assert np.array_equal(uf, np.floor(uf)) and (uf.astype(np.int64) & 1).any()
+    # the mantissa mode changes the mapping, not the consumption
+    a, b = state_io.create("x256++", seed=[6]), state_io.create("x256++", seed=[6])
+    b.set_full_mantissa(True)
+    assert not torch.equal(a.fill("u01", {}, 5000), b.fill("u01", {}, 5000))
+    assert a.next_u64() == b.next_u64()
+    # two u01f consume one word
+    a, b = state_io.create("pcg64", seed=[8]), state_io.create("pcg64", seed=[8])
+    words = [a.next_u64() for _ in range(2049)]
+    b.fill("u01f", {}, 4096)
+    assert b.next_u64() == words[2048]
+    # a failed draw preserves the stream position and records the reference's message
+    r = state_io.create("x256++", seed=[42])
+    expect = [state_io.create("x256++", seed=[42]).next_u64()]
+    with pytest.raises(ValueError):
+        r.fill("gamma", {"alpha": -1.0}, 1000)
+    assert r.last_error == "gamma shape must be > 0"
+    assert r.next_u64() == expect[0]
+    # the fill surface
+    r = state_io.create("x256++", seed=[43])
+    assert r.fill("norm", {}, 0).numel() == 0
+    v = _np(r.fill("norm", {"mu": 100.0, "var": 0.01}, 4096))
+    assert ((v > 99.0) & (v < 101.0)).all()
+    with pytest.raises(ValueError, match="unknown"):
+        r.fill("zipf", {}, 1)
+    with pytest.raises(ValueError, match="bad parameters"):
+        r.fill("norm", {"location": 3.0}, 1)
+    with pytest.raises(ValueError, match="draw count"):
+        r.fill("norm", {}, -1)
+    # replays
+    for dist, params in (("norm", {}), ("exp", {}), ("gamma", {"alpha": 0.5}), ("beta", {"a": 2.0, "b": 3.0})):
+        x = state_io.create("pcg64", seed=[1, 2]).fill(dist, params, 3000)
+        y = state_io.create("pcg64", seed=[1, 2]).fill(dist, params, 3000)
+        assert torch.equal(x, y), dist
+    # mvn: layouts transpose each other; a rank-one covariance ties the coordinates; rejections
+    cov = [[2.0, 0.3], [0.3, 1.0]]
+    x = _np(state_io.create("x256++", seed=[35]).mvn([1.0, -1.0], cov, n=500, layout="n_d"))
+    y = _np(state_io.create("x256++", seed=[35]).mvn([1.0, -1.0], cov, n=500, layout="d_n"))
+    assert x.shape == (500, 2) and y.shape == (2, 500) and np.array_equal(x, y.T)
+    d = _np(state_io.create("x256++", seed=[31]).mvn([0.0, 0.0], [[1.0, 1.0], [1.0, 1.0]], n=200))
+    assert np.allclose(d[:, 0], d[:, 1], rtol=0.0, atol=1e-12)
+    with pytest.raises(ValueError, match="positive semidefinite"):
+        state_io.create("x256++", seed=[32]).mvn([0.0, 0.0], [[1.0, 2.0], [2.0, 1.0]])
+    with pytest.raises(ValueError, match="symmetric"):
+        state_io.create("x256++", seed=[33]).mvn([0.0, 0.0], [[1.0, 0.5], [0.1, 1.0]])
+    with pytest.raises(ValueError, match="length-d mean"):
+        state_io.create("x256++", seed=[34]).mvn([0.0, 0.0], [[1.0]])
