@@ -1012,3 +1012,56 @@ def test_reference_behaviours_on_the_device_path():
         state_io.create("x256++", seed=[33]).mvn([0.0, 0.0], [[1.0, 0.5], [0.1, 1.0]])
     with pytest.raises(ValueError, match="length-d mean"):
         state_io.create("x256++", seed=[34]).mvn([0.0, 0.0], [[1.0]])
+
+
+def test_reference_discrete_behaviours_on_the_device_path():
+    """The properties of the reference's bounded-integer tests (pkg/tests/test_discrete.py:51-147,
+    :245-290) on device fills: power-of-two bounds never reject and equal (w b) >> 64, the
+    pass-throughs (b = 0, 1, 2^64), sub-64-bit draws pairing into half words, ranges and spans
+    of every named law, light uniformity, and validation that consumes nothing."""
+    n = 1 << 16
+    raw = _np(state_io.create("x256++", seed=[51]).fill("uint64", {}, n))
+    for k in (1, 4, 16, 40, 63):  # power-of-two bounds: one word per sample, value = high bits
+        r = state_io.create("x256++", seed=[51])
+        v = _np(r.fill("uint64", {"b": 1 << k}, n))
+        assert np.array_equal(v, raw >> np.uint64(64 - k))
+        assert r.next_u64() == int(_np(state_io.create("x256++", seed=[51]).fill("uint64", {}, n + 1))[n])
+    for b in (0, 1 << 64):  # pass-throughs
+        assert np.array_equal(_np(state_io.create("x256++", seed=[51]).fill("uint64", {"b": b}, n)), raw)
+    r = state_io.create("x256++", seed=[51])
+    assert not _np(r.fill("uint64", {"b": 1}, n)).any()  # b = 1 still consumes its words
+    assert r.next_u64() == int(_np(state_io.create("x256++", seed=[51]).fill("uint64", {}, n + 1))[n])
+    # sub-64-bit draws pair into half words: 2 n draws of width <= 32 consume n words
+    r = state_io.create("pcg64", seed=[61])
+    words = _np(state_io.create("pcg64", seed=[61]).fill("uint64", {}, n + 1))
+    v8 = _np(r.fill("uint8", {}, 2 * n))
+    assert np.array_equal(v8[0::2], (words[:n] & np.uint64(0xFF)).astype(v8.dtype))
+    assert np.array_equal(v8[1::2], ((words[:n] >> np.uint64(32)) & np.uint64(0xFF)).astype(v8.dtype))
+    assert r.next_u64() == int(words[n])
+    # ranges and spans
+    r = state_io.create("pcg64", seed=[91])
+    for dist, b in (("uint8", 6), ("uint16", 1000), ("uint32", 3)):
+        v = _np(r.fill(dist, {"b": b}, 50000))
+        assert v.min() == 0 and v.max() == b - 1
+    v = _np(r.fill("int", {"m": -5, "n": 5}, 50000))
+    assert set(np.unique(v).tolist()) == set(range(-5, 6))
+    v = _np(r.fill("long_long", {}, 50000))
+    assert (v < 0).any() and (v > 0).any()
+    v = _np(r.fill("long_long", {"m": -(1 << 63), "n": (1 << 63) - 1}, 8))  # full span: offset pass-through
+    assert v.dtype == np.int64
+    # light uniformity (chi-square of 10 cells over 2^20 draws)
+    c = np.bincount(_np(state_io.create("x256++", seed=[84]).fill("uint64", {"b": 10}, 1 << 20)).astype(np.int64),
+                    minlength=10)
+    e = (1 << 20) / 10.0
+    assert (((c - e) ** 2) / e).sum() < 45.0  # chi2(9) survival ~ 1e-6
+    # validation consumes nothing
+    r = state_io.create("x256++", seed=[93])
+    first = state_io.create("x256++", seed=[93]).next_u64()
+    for dist, params, msg in (("uint8", {"b": 257}, "bound"), ("uint64", {"b": -1}, "bound"),
+                              ("int", {"m": 5, "n": 4}, "does not fit"), ("int", {"m": 0, "n": 1 << 31}, "does not fit")):
+        with pytest.raises(ValueError, match=msg):
+            r.fill(dist, params, 100)
+    with pytest.raises(ValueError, match="draw count"):
+        r.fill("uint64", {}, -1)
+    assert r.fill("uint64", {}, 0).numel() == 0
+    assert r.next_u64() == first
